@@ -1,0 +1,503 @@
+// host.h — host-side plan/level machinery shared by capi.cu (pipeline) and
+// stages.cu (per-stage parity entry points).
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "hwflow_c.h"
+#include "launch.h"
+
+using namespace hwf;
+
+namespace hwf_host {
+
+struct CudaError : std::runtime_error {
+  explicit CudaError(const std::string& m) : std::runtime_error(m) {}
+};
+struct InvalidArg : std::runtime_error {
+  explicit InvalidArg(const std::string& m) : std::runtime_error(m) {}
+};
+struct Diverged : std::runtime_error {
+  explicit Diverged(const std::string& m) : std::runtime_error(m) {}
+};
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess)                                                                 \
+      throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));                    \
+  } while (0)
+
+// ---- device memory ------------------------------------------------------------
+struct DevMem {
+  std::vector<void*> ptrs;
+  template <class T>
+  T* alloc(size_t n) {
+    if (n == 0) n = 1;
+    void* p = nullptr;
+    CK(cudaMalloc(&p, n * sizeof(T)));
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  void release() {
+    for (void* p : ptrs) cudaFree(p);
+    ptrs.clear();
+  }
+  ~DevMem() { release(); }
+};
+
+inline Params to_params(const hwf_energy_params& p) {
+  Params q;
+  std::memcpy(&q, &p, sizeof(q));
+  return q;
+}
+
+inline int gn_for_level(const hwf_schedule& S, int l) {  // solver.hpp:30-34
+  if (S.n_gn_per_level > 0) return S.gn_per_level[std::min(l, S.n_gn_per_level - 1)];
+  return l <= 1 ? 2 : 5;
+}
+
+// One level's device state for a batch of B pairs.
+struct LevelDev {
+  int w = 0, h = 0, gw = 0, gh = 0, step = 0, ncx = 0, ncy = 0, tcx = 0, tcy = 0, rp = 0;
+  int ntx = 0, nty = 0, nxm = 0, nym = 0, tile = 0;
+  size_t N = 0, G = 0, C = 0;
+  double *img = nullptr, *illum = nullptr, *base = nullptr, *delta = nullptr, *total = nullptr;
+  double *nodew = nullptr, *half = nullptr, *cells = nullptr, *sys = nullptr, *xa = nullptr, *xb = nullptr,
+         *hm = nullptr;
+  uint8_t *vis = nullptr, *W = nullptr, *occ = nullptr;
+  int n_pix_cta = 0, n_node_cta = 0;
+
+  void dims(int w_, int h_, int step_, int tile_px) {
+    w = w_;
+    h = h_;
+    step = step_;
+    gw = std::max((w - 1 + step - 1) / step + 1, 2);  // warp_grid.cpp:11-14
+    gh = std::max((h - 1 + step - 1) / step + 1, 2);
+    ncx = gw - 1;
+    ncy = gh - 1;
+    N = static_cast<size_t>(w) * h;
+    G = static_cast<size_t>(gw) * gh;
+    C = static_cast<size_t>(ncx) * ncy;
+    tcx = pixel_tile_cells_x(step);
+    tcy = pixel_tile_cells_y(step);
+    rp = pixel_smem_pitch(step);
+    n_pix_cta = ((ncx + tcx - 1) / tcx) * ((ncy + tcy - 1) / tcy);
+    n_node_cta = node_ctas(static_cast<int>(G));
+    tile = tile_px;
+    if (tile_px > 0) {  // solver.cpp:385-388
+      ntx = ((gw - 1) * step) / tile_px + 1;
+      nty = ((gh - 1) * step) / tile_px + 1;
+      nxm = (tile_px + step - 1) / step;
+      nym = nxm;
+    }
+  }
+  void alloc_solver(DevMem& m, int B, bool schwarz) {
+    base = m.alloc<double>(B * G * 6);
+    delta = m.alloc<double>(B * G * 6);
+    total = m.alloc<double>(B * G * 6);
+    nodew = m.alloc<double>(B * G);
+    half = m.alloc<double>(B * N);
+    cells = m.alloc<double>(B * C * kCellStride);
+    sys = m.alloc<double>(B * G * kSysStride);
+    W = m.alloc<uint8_t>(B * N);
+    vis = m.alloc<uint8_t>(B * N);
+    if (schwarz) {
+      xa = m.alloc<double>(B * G * 6);
+      xb = m.alloc<double>(B * G * 6);
+    }
+  }
+};
+
+struct Scratch {  // shared across levels, sized for the finest
+  int2* q = nullptr;
+  float* Z = nullptr;
+  uint8_t* bad = nullptr;
+  unsigned long long* zbuf = nullptr;
+  uint8_t* degen = nullptr;
+  double *resid = nullptr, *tmp = nullptr;
+  double *px = nullptr, *pr = nullptr, *pz = nullptr, *pp = nullptr, *pap = nullptr;
+  void alloc(DevMem& m, int B, size_t N, size_t G, bool occ, bool illum, bool pcg) {
+    if (occ) {
+      q = m.alloc<int2>(B * N * 4);
+      Z = m.alloc<float>(B * N);
+      bad = m.alloc<uint8_t>(B * N);
+      zbuf = m.alloc<unsigned long long>(B * N * 4);
+      degen = m.alloc<uint8_t>(B * N * 4);
+    }
+    if (illum) {
+      resid = m.alloc<double>(B * N * 2);
+      tmp = m.alloc<double>(B * N * 2);
+    }
+    if (pcg) {
+      px = m.alloc<double>(B * G * 6);
+      pr = m.alloc<double>(B * G * 6);
+      pz = m.alloc<double>(B * G * 6);
+      pp = m.alloc<double>(B * G * 6);
+      pap = m.alloc<double>(B * G * 6);
+    }
+  }
+};
+
+struct Energies {  // partial buffer [B][nslots][cap][5] and reduced [B][nslots][5]
+  int nslots = 0, cap = 0;
+  double* part = nullptr;
+  double* red = nullptr;
+  long long pair_stride() const { return static_cast<long long>(nslots) * cap * kNumEnergy; }
+  double* slot(int s) const { return part + static_cast<size_t>(s) * cap * kNumEnergy; }
+};
+
+struct Launches {
+  int count = 0;
+  std::vector<cudaEvent_t>* ev = nullptr;  // pixel-kernel timing events (optional)
+  std::vector<double>* bytes = nullptr;
+};
+
+// Algorithmic bytes of one k_pixel<LIN> launch: every
+// input read once, every output written once.
+inline double pixel_bytes(const LevelDev& d, int B, bool illum) {
+  const double perpix = 4 * 8.0 + (illum ? 4 * 8.0 : 0.0) + 1 + 1 + 1 + 8;
+  return B * (d.N * perpix + d.G * 48.0 + d.C * kCellStride * 8.0);
+}
+
+// The nonlinear loop of one level (solver.cpp:484-532) for a batch.
+inline void record_gn_level(LevelDev& d, int B, const hwf_energy_params& P, const hwf_schedule& S, const double* dF,
+                     int gn, const Energies& E, int slot_base, Scratch& sc, int* flags, cudaStream_t st,
+                     Launches& L) {
+  PixArgs pa{};
+  pa.w = d.w; pa.h = d.h; pa.gw = d.gw; pa.gh = d.gh; pa.step = d.step; pa.ncx = d.ncx; pa.ncy = d.ncy;
+  pa.tcx = d.tcx; pa.tcy = d.tcy; pa.rp = d.rp;
+  pa.img = d.img; pa.illum = d.illum; pa.vis4 = d.vis; pa.W = d.W; pa.total = d.total; pa.half = d.half;
+  pa.cells = d.cells; pa.ep_pair = E.pair_stride(); pa.flags = flags; pa.P = to_params(P);
+  pa.active = S.active_fields; pa.refresh = 1;
+  NodeArgs na{};
+  na.w = d.w; na.h = d.h; na.gw = d.gw; na.gh = d.gh; na.step = d.step; na.ncx = d.ncx; na.ncy = d.ncy;
+  na.half = d.half; na.node_w = d.nodew; na.total = d.total; na.delta = d.delta; na.cells = d.cells;
+  na.sys = d.sys; na.ep_pair = E.pair_stride(); na.ep_base = d.n_pix_cta; na.flags = flags;
+  na.P = to_params(P); na.F = dF; na.active = S.active_fields; na.lm = S.lm_lambda; na.refresh = 1;
+  for (int it = 0; it < gn; ++it) {
+    pa.ep_new = E.slot(slot_base + 2 * it);
+    pa.ep_old = it > 0 ? E.slot(slot_base + 2 * (it - 1) + 1) : nullptr;
+    if (L.ev) CK(cudaEventRecordWithFlags((*L.ev)[2 * L.bytes->size()], st, cudaEventRecordExternal));
+    launch_pixel(true, pa, B, st);
+    if (L.ev) {
+      CK(cudaEventRecordWithFlags((*L.ev)[2 * L.bytes->size() + 1], st, cudaEventRecordExternal));
+      L.bytes->push_back(pixel_bytes(d, B, d.illum != nullptr));
+    }
+    na.ep_new = pa.ep_new;
+    na.ep_old = pa.ep_old;
+    launch_node(true, na, B, st);
+    L.count += 2;
+    if (S.subdomain_px > 0) {
+      SwzArgs sa{};
+      sa.gw = d.gw; sa.gh = d.gh; sa.step = d.step; sa.tile = d.tile; sa.ntx = d.ntx; sa.nty = d.nty;
+      sa.nxm = d.nxm; sa.nym = d.nym; sa.sys = d.sys; sa.delta = d.delta; sa.total = d.total; sa.base = d.base;
+      sa.active = S.active_fields; sa.pcg_iters = S.pcg_iters; sa.flags = flags;
+      for (int s = 0; s < S.patch_iters; ++s) {
+        sa.pub = s == 0 ? nullptr : (s & 1 ? d.xb : d.xa);
+        sa.next = s & 1 ? d.xa : d.xb;
+        sa.last = s == S.patch_iters - 1;
+        launch_schwarz(sa, B, st);
+        L.count += 1;
+      }
+    } else {
+      PcgArgs ga{};
+      ga.gw = d.gw; ga.gh = d.gh; ga.iters = S.pcg_iters; ga.sys = d.sys;
+      ga.x = sc.px; ga.r = sc.pr; ga.z = sc.pz; ga.p = sc.pp; ga.ap = sc.pap; ga.trace = nullptr;
+      ga.update = 1; ga.delta = d.delta; ga.total = d.total; ga.base = d.base; ga.active = S.active_fields;
+      ga.flags = flags;
+      launch_pcg_global(ga, B, st);
+      L.count += 1;
+    }
+  }
+  if (gn > 0) {  // E_after of the last iteration (solver.cpp:523-528)
+    pa.refresh = 0;
+    pa.ep_new = E.slot(slot_base + 2 * (gn - 1) + 1);
+    pa.ep_old = nullptr;
+    launch_pixel(false, pa, B, st);
+    na.refresh = 0;
+    na.ep_new = pa.ep_new;
+    na.ep_old = nullptr;
+    launch_node(false, na, B, st);
+    L.count += 2;
+  }
+}
+
+// ---- the batched plan (one CUDA graph per configuration) ------------------------
+struct Plan {
+  int B = 0, w = 0, h = 0, dtype = 0;
+  hwf_energy_params P{};
+  hwf_schedule S{};
+  bool hasF = false;
+  double F[9] = {};
+  unsigned outmask = 0;  // 1 s, 2 m, 4 d, 8 disparity
+  bool profile = false;
+
+  int L = 0;
+  LevelDev lv[HWF_MAX_LEVELS];
+  int gn[HWF_MAX_LEVELS] = {};
+  int slot_base[HWF_MAX_LEVELS] = {};
+  DevMem mem;
+  void* in = nullptr;
+  double* dF = nullptr;
+  Scratch sc;
+  Energies E;
+  int* flags = nullptr;
+  double *o_s = nullptr, *o_m = nullptr, *o_d = nullptr, *o_disp = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int launches = 0;
+  std::vector<cudaEvent_t> ev;
+  std::vector<double> ev_bytes;
+
+  bool matches(int B_, int w_, int h_, int dt, const hwf_energy_params& P_, const hwf_schedule& S_, const double* F_,
+               unsigned om, bool prof) const {
+    if (B != B_ || w != w_ || h != h_ || dtype != dt || outmask != om || profile != prof) return false;
+    if (std::memcmp(&P, &P_, sizeof(P)) || std::memcmp(&S, &S_, sizeof(S))) return false;
+    if (hasF != (F_ != nullptr)) return false;
+    return !F_ || std::memcmp(F, F_, sizeof(F)) == 0;
+  }
+  ~Plan() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+
+  void build(cudaStream_t st) {
+    int dims[4 * HWF_MAX_LEVELS];
+    if (hwf_level_dims(w, h, S.levels, S.grid_step, &L, dims) != HWF_OK) throw InvalidArg("bad level dims");
+    size_t cap = 0;
+    int nslots = 0;
+    for (int l = 0; l < L; ++l) {
+      lv[l].dims(dims[4 * l], dims[4 * l + 1], S.grid_step, S.subdomain_px);
+      gn[l] = gn_for_level(S, l);
+      if (gn[l] > HWF_MAX_GN) throw InvalidArg("gn_per_level exceeds HWF_MAX_GN");
+      slot_base[l] = nslots;
+      nslots += 2 * gn[l];
+      cap = std::max(cap, static_cast<size_t>(lv[l].n_pix_cta + lv[l].n_node_cta));
+    }
+    const size_t N0 = lv[0].N;
+    in = dtype == HWF_DTYPE_U8 ? static_cast<void*>(mem.alloc<uint8_t>(B * 4 * N0))
+                               : static_cast<void*>(mem.alloc<double>(B * 4 * N0));
+    for (int l = 0; l < L; ++l) {
+      LevelDev& d = lv[l];
+      d.img = mem.alloc<double>(B * 4 * d.N);
+      d.alloc_solver(mem, B, S.subdomain_px > 0);
+      d.occ = mem.alloc<uint8_t>(B * d.N);
+      if (l < L - 1) d.illum = mem.alloc<double>(B * 4 * d.N);
+      if (l > 0) d.hm = mem.alloc<double>(B * 2 * d.N);
+    }
+    sc.alloc(mem, B, N0, lv[0].G, true, L > 1, S.subdomain_px <= 0);
+    E.nslots = std::max(nslots, 1);
+    E.cap = static_cast<int>(cap);
+    E.part = mem.alloc<double>(static_cast<size_t>(B) * E.pair_stride());
+    E.red = mem.alloc<double>(static_cast<size_t>(B) * E.nslots * kNumEnergy);
+    flags = mem.alloc<int>(B);
+    if (hasF) {
+      dF = mem.alloc<double>(9);
+      CK(cudaMemcpy(dF, F, sizeof(F), cudaMemcpyHostToDevice));
+    }
+    if (outmask & 1) o_s = mem.alloc<double>(B * N0 * 2);
+    if (outmask & 2) o_m = mem.alloc<double>(B * N0 * 2);
+    if (outmask & 4) o_d = mem.alloc<double>(B * N0 * 2);
+    if (outmask & 8) o_disp = mem.alloc<double>(B * N0);
+    if (profile) {
+      int total_gn = 0;
+      for (int l = 0; l < L; ++l) total_gn += gn[l];
+      ev.resize(2 * std::max(total_gn, 1));
+      for (auto& e : ev) CK(cudaEventCreate(&e));
+    }
+    // capture the pipeline into one graph
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    try {
+      record(st);
+    } catch (...) {
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(st, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    CK(cudaStreamEndCapture(st, &graph));
+    CK(cudaGraphInstantiate(&exec, graph, 0));
+  }
+
+  void record(cudaStream_t st) {
+    Launches LC;
+    ev_bytes.clear();
+    if (profile) {
+      LC.ev = &ev;
+      LC.bytes = &ev_bytes;
+    }
+    CK(cudaMemsetAsync(E.part, 0, sizeof(double) * B * E.pair_stride(), st));
+    CK(cudaMemsetAsync(flags, 0, sizeof(int) * B, st));
+    // pyramid (image.cpp:177-185)
+    launch_pyr_in(in, dtype, lv[0].img, static_cast<long long>(B) * 4 * lv[0].N, st);
+    LC.count++;
+    for (int l = 1; l < L; ++l) {
+      launch_pyr_down(lv[l - 1].img, lv[l - 1].w, lv[l - 1].h, lv[l].img, lv[l].w, lv[l].h, 4 * B, st);
+      LC.count++;
+    }
+    for (int l = L - 1; l >= 0; --l) {
+      LevelDev& d = lv[l];
+      if (l == L - 1) {  // pin C.6
+        launch_init_coarse(d.base, d.total, d.delta, static_cast<int>(d.G), B, S.coarse_s_offset[0],
+                           S.coarse_s_offset[1], st);
+        CK(cudaMemsetAsync(d.vis, 0x0F, B * d.N, st));
+        LC.count++;
+      } else {  // prolongation
+        const LevelDev& c = lv[l + 1];
+        launch_prolong_grid(c.gw, c.gh, d.gw, d.gh, d.step, c.total, d.base, d.total, d.delta, B, st);
+        launch_prolong_maps(c.w, c.h, d.w, d.h, c.occ, c.hm, d.vis, d.illum, B, st);
+        LC.count += 2;
+      }
+      CK(cudaMemsetAsync(d.W, 1, B * d.N, st));
+      CK(cudaMemsetAsync(d.nodew, 0, sizeof(double) * B * d.G, st));
+      record_gn_level(d, B, P, S, dF, gn[l], E, slot_base[l], sc, flags, st, LC);
+      launch_occlusion(d.w, d.h, d.gw, d.gh, d.step, d.total, B, sc.q, sc.Z, sc.bad, sc.zbuf, sc.degen, d.occ, st);
+      LC.count += 3;
+      if (l > 0) {
+        launch_illumination(d.w, d.h, d.gw, d.gh, d.step, d.img, d.total, d.occ, B, sc.resid, sc.tmp, d.hm, st);
+        LC.count += 3;
+      }
+    }
+    if (outmask & 15) {
+      launch_dense(lv[0].w, lv[0].h, lv[0].gw, lv[0].gh, lv[0].step, lv[0].total, B, o_s, o_m, o_d, o_disp, st);
+      LC.count++;
+    }
+    launch_energy_reduce(E.part, E.nslots, E.cap, B, E.red, flags, st);
+    LC.count++;
+    CK(cudaGetLastError());
+    launches = LC.count;
+  }
+};
+
+}  // namespace hwf_host
+
+struct hwf_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  std::unique_ptr<hwf_host::Plan> plan;
+  bool profile = false;
+};
+
+namespace hwf_host {
+
+template <class Fn>
+int guard(hwf_ctx* ctx, Fn&& fn) {
+  try {
+    if (!ctx) throw InvalidArg("null context");
+    CK(cudaSetDevice(ctx->device));
+    fn();
+    return HWF_OK;
+  } catch (const InvalidArg& e) {
+    if (ctx) ctx->err = e.what();
+    return HWF_EINVAL;
+  } catch (const Diverged& e) {
+    if (ctx) ctx->err = e.what();
+    return HWF_EDIVERGED;
+  } catch (const CudaError& e) {
+    if (ctx) ctx->err = e.what();
+    return HWF_ECUDA;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->err = e.what();
+    return HWF_EINVAL;
+  }
+}
+
+inline void check_params(const hwf_energy_params* P, const hwf_schedule* S, const double* F) {
+  if (!P || !S) throw InvalidArg("null params/schedule");
+  if (hwf_validate_params(P) != HWF_OK) throw InvalidArg("energy weights must be >= 0 and eps_huber > 0");
+  if (P->w_epi > 0.0 && !F) throw InvalidArg("epipolar term enabled without a fundamental matrix");
+  if (S->grid_step < 1 || S->grid_step > 32) throw InvalidArg("grid_step must be in [1, 32] on the device");
+  if (S->subdomain_px > 0 && (S->subdomain_px + S->grid_step - 1) / S->grid_step > 5)
+    throw InvalidArg("subdomain tile must hold <= 5x5 nodes on the device");
+  if (S->pcg_iters < 0 || S->patch_iters < 0) throw InvalidArg("negative iteration count");
+}
+
+inline void upload_frames(Plan& p, int n, const hwf_frame4* fr, cudaStream_t st) {
+  const size_t N = static_cast<size_t>(p.w) * p.h;
+  const size_t esz = p.dtype == HWF_DTYPE_U8 ? 1 : 8;
+  // fast path: all 4n planes contiguous in one host allocation
+  bool contiguous = true;
+  const char* base = static_cast<const char*>(fr[0].plane[0]);
+  for (int i = 0; i < n && contiguous; ++i)
+    for (int e = 0; e < 4; ++e)
+      contiguous = contiguous && static_cast<const char*>(fr[i].plane[e]) == base + (4 * static_cast<size_t>(i) + e) * N * esz;
+  if (contiguous) {
+    CK(cudaMemcpyAsync(p.in, base, 4 * n * N * esz, cudaMemcpyHostToDevice, st));
+    return;
+  }
+  for (int i = 0; i < n; ++i)
+    for (int e = 0; e < 4; ++e)
+      CK(cudaMemcpyAsync(static_cast<char*>(p.in) + (4 * static_cast<size_t>(i) + e) * N * esz, fr[i].plane[e],
+                         N * esz, cudaMemcpyHostToDevice, st));
+}
+
+inline Plan& get_plan(hwf_ctx* ctx, int n, int w, int h, int dtype, const hwf_energy_params* P, const hwf_schedule* S,
+               const double* F, unsigned outmask) {
+  if (ctx->plan && ctx->plan->matches(n, w, h, dtype, *P, *S, F, outmask, ctx->profile)) return *ctx->plan;
+  ctx->plan.reset();
+  CK(cudaStreamSynchronize(ctx->stream));
+  auto p = std::make_unique<Plan>();
+  p->B = n;
+  p->w = w;
+  p->h = h;
+  p->dtype = dtype;
+  p->P = *P;
+  p->S = *S;
+  p->hasF = F != nullptr;
+  if (F) std::memcpy(p->F, F, sizeof(p->F));
+  p->outmask = outmask;
+  p->profile = ctx->profile;
+  p->build(ctx->stream);
+  ctx->plan = std::move(p);
+  return *ctx->plan;
+}
+
+inline void finish_stats(const Plan& p, int n, hwf_stats* stats, std::vector<int>& flags) {
+  std::vector<double> red(static_cast<size_t>(p.B) * p.E.nslots * kNumEnergy);
+  flags.resize(p.B);
+  // (the stream is synchronous with these blocking copies)
+  CK(cudaMemcpy(red.data(), p.E.red, red.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(flags.data(), p.flags, sizeof(int) * p.B, cudaMemcpyDeviceToHost));
+  if (!stats) return;
+  const hwf_energy_params& P = p.P;
+  for (int i = 0; i < n; ++i) {
+    hwf_stats& s = stats[i];
+    std::memset(&s, 0, sizeof(s));
+    s.levels_used = p.L;
+    for (int l = 0; l < p.L; ++l) {
+      s.gn_iters[l] = p.gn[l];
+      for (int it = 0; it < p.gn[l]; ++it)
+        for (int k = 0; k < 2; ++k) {
+          const double* e = red.data() + (static_cast<size_t>(i) * p.E.nslots + p.slot_base[l] + 2 * it + k) * kNumEnergy;
+          const double tot = P.w_photo * e[0] + P.w_grad * e[1] + P.w_reg * (P.w_smooth * e[2] + P.w_epi * e[3] + P.w_mag * e[4]);
+          (k == 0 ? s.energy_before : s.energy_after)[l][it] = tot;
+        }
+    }
+  }
+}
+
+inline void raise_on_flags(const std::vector<int>& flags, int n) {
+  std::string msg;
+  for (int i = 0; i < n; ++i)
+    if (flags[i]) {
+      if (!msg.empty()) msg += "; ";
+      msg += "pair " + std::to_string(i) + ":";
+      if (flags[i] & kFlagJacobian) msg += " non-finite Jacobian";
+      if (flags[i] & kFlagCurvature) msg += " PCG: non-positive curvature, system not SPD";
+      if (flags[i] & kFlagGrowth) msg += " PCG: preconditioned residual grew by more than 10x";
+      if (flags[i] & kFlagStep) msg += " non-finite Gauss-Newton update";
+      if (flags[i] & kFlagEnergy) msg += " non-finite energy";
+    }
+  if (!msg.empty()) throw Diverged(msg);
+}
+
+}  // namespace hwf_host

@@ -1,0 +1,123 @@
+// launch.h — kernel argument blocks and host launchers (one translation unit per kernel family).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "device.cuh"
+
+namespace hwf {
+
+// divergence flag bits (per pair), mirroring the reference's SolverDivergence sites
+enum : int {
+  kFlagJacobian = 1,   // solver.cpp:116-118
+  kFlagCurvature = 2,  // solver.cpp:345-346
+  kFlagGrowth = 4,     // solver.cpp:353-355
+  kFlagStep = 8,       // solver.cpp:515-516
+  kFlagEnergy = 16,    // energy.cpp:225-226, solver.cpp:526-527
+};
+
+struct PixArgs {
+  int w, h, gw, gh, step, ncx, ncy, tcx, tcy, rp;
+  const double* img;    // [B][4][N]
+  const double* illum;  // [B][4][N] or null
+  const uint8_t* vis4;  // [B][N]
+  uint8_t* W;           // [B][N] in: current bits; out: refreshed bits (refresh)
+  const double* total;  // [B][G][6]
+  double* half;         // [B][N] (lin)
+  double* cells;        // [B][C][234] (lin)
+  double* ep_new;       // energy partials with the refreshed W; [pair stride ep_pair]
+  double* ep_old;       // energy partials with the incoming W (nullable)
+  long long ep_pair;    // doubles between pairs in the partial buffer
+  int* flags;
+  Params P;
+  uint32_t active;
+  int refresh;
+};
+
+struct NodeArgs {
+  int w, h, gw, gh, step, ncx, ncy;
+  const double* half;   // [B][N]
+  double* node_w;       // [B][G]
+  const double* total;  // [B][G][6]
+  const double* delta;  // [B][G][6]
+  const double* cells;  // [B][C][234]
+  double* sys;          // [B][G][120]
+  double* ep_new;
+  double* ep_old;
+  long long ep_pair;
+  int ep_base;          // first partial slot used by node CTAs
+  int* flags;
+  Params P;
+  const double* F;      // 9 doubles (device) or null
+  uint32_t active;
+  double lm;
+  int refresh;
+};
+
+struct SwzArgs {
+  int gw, gh, step, tile, ntx, nty, nxm, nym;
+  const double* sys;    // [B][G][120]
+  const double* pub;    // [B][G][6] or null (first sweep: zero)
+  double* next;         // [B][G][6]
+  int last;             // fuse the Gauss-Newton update (solver.cpp:518-521)
+  double* delta;
+  double* total;
+  const double* base;
+  uint32_t active;
+  int pcg_iters;
+  int* flags;
+};
+
+struct PcgArgs {
+  int gw, gh, iters;
+  const double* sys;
+  double *x, *r, *z, *p, *ap;  // [B][6G] scratch
+  double* trace;               // [B][iters+1] or null
+  int update;                  // apply delta += x, total = base + delta
+  double* delta;
+  double* total;
+  const double* base;
+  uint32_t active;
+  int* flags;
+};
+
+// once per device, outside any stream capture
+void init_pixel_attributes();
+void init_maps_constants();
+
+// pixel.cu
+int pixel_tile_cells_x(int step);
+int pixel_tile_cells_y(int step);
+int pixel_smem_pitch(int step);
+size_t pixel_smem_bytes(int step);
+void launch_pixel(bool lin, const PixArgs& a, int B, cudaStream_t s);
+int node_ctas(int G);
+void launch_node(bool lin, const NodeArgs& a, int B, cudaStream_t s);
+
+// solve.cu
+void launch_schwarz(const SwzArgs& a, int B, cudaStream_t s);
+void launch_pcg_global(const PcgArgs& a, int B, cudaStream_t s);
+
+// maps.cu
+void launch_pyr_in(const void* src, int dtype, double* dst, long long n, cudaStream_t s);
+void launch_pyr_down(const double* src, int w, int h, double* dst, int ow, int oh, int planes,
+                     cudaStream_t s);
+void launch_init_coarse(double* base, double* total, double* delta, int G, int B, double ox,
+                        double oy, cudaStream_t s);
+void launch_occlusion(int w, int h, int gw, int gh, int step, const double* total, int B,
+                      int2* q, float* Z, uint8_t* bad, unsigned long long* zbuf, uint8_t* degen,
+                      uint8_t* vis_out, cudaStream_t s);
+void launch_illumination(int w, int h, int gw, int gh, int step, const double* img,
+                         const double* total, const uint8_t* vis, int B, double* resid,
+                         double* tmp, double* hm, cudaStream_t s);
+void launch_prolong_grid(int gwc, int ghc, int gwf, int ghf, int step, const double* total_c,
+                         double* base_f, double* total_f, double* delta_f, int B, cudaStream_t s);
+void launch_prolong_maps(int wc, int hc, int wf, int hf, const uint8_t* vis_c, const double* hm_c,
+                         uint8_t* vis_f, double* illum_f, int B, cudaStream_t s);
+void launch_dense(int w, int h, int gw, int gh, int step, const double* total, int B, double* s_out,
+                  double* m_out, double* d_out, double* disp_out, cudaStream_t s);
+void launch_energy_reduce(const double* ep, int nslots, int cap, int B, double* out, int* flags,
+                          cudaStream_t s);
+
+}  // namespace hwf

@@ -1,0 +1,379 @@
+// maps.cu — pyramid, occlusion, illumination, prolongation, dense output and
+// the deterministic energy reduction.
+//
+// Bit-exact stages (pyramid, occlusion) round every operation explicitly
+// (__dadd_rn/__dmul_rn/__ddiv_rn/__dsqrt_rn) in the reference's order so that
+// they match the -ffp-contract=off CPU oracle bit for bit.
+#include <cmath>
+
+#include "launch.h"
+
+namespace hwf {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kZbufSpanPx = 32;   // oracle/hierarchy.cpp pin C.2
+constexpr double kDepthTol = 1e-4;
+
+// ---- pyramid (image.cpp:100-122, 177-185) -----------------
+__global__ void k_pyr_in(const void* __restrict__ src, int dtype, double* __restrict__ dst, long long n) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  if (dtype == HWF_DTYPE_U8) {
+    dst[i] = __ddiv_rn(static_cast<double>(static_cast<const uint8_t*>(src)[i]), 255.0);
+  } else {
+    const double v = static_cast<const double*>(src)[i];
+    dst[i] = fmin(1.0, fmax(0.0, v));
+  }
+}
+
+__global__ void k_pyr_down(const double* __restrict__ src, int w, int h, double* __restrict__ dst,
+                           int ow, int oh) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+  const int plane = blockIdx.z;
+  if (x >= ow) return;
+  const double* S = src + static_cast<size_t>(plane) * w * h;
+  double sum = 0.0;
+  int cnt = 0;
+  for (int dy = 0; dy < 2; ++dy)
+    for (int dx = 0; dx < 2; ++dx) {
+      const int sx = 2 * x + dx, sy = 2 * y + dy;
+      if (sx < w && sy < h) {
+        sum = __dadd_rn(sum, S[static_cast<size_t>(sy) * w + sx]);
+        ++cnt;
+      }
+    }
+  dst[static_cast<size_t>(plane) * ow * oh + static_cast<size_t>(y) * ow + x] = __ddiv_rn(sum, static_cast<double>(cnt));
+}
+
+__global__ void k_init_coarse(double* base, double* total, double* delta, long long n_nodes, double ox, double oy) {
+  const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (t >= 6 * n_nodes) return;
+  const int c = static_cast<int>(t % 6);
+  const double v = c == 0 ? __dadd_rn(0.0, ox) : (c == 1 ? __dadd_rn(0.0, oy) : 0.0);
+  base[t] = v;
+  total[t] = v;
+  delta[t] = 0.0;
+}
+
+// ---- occlusion (pin C.2 in oracle/hierarchy.cpp) ---------
+__global__ void k_occ_project(int w, int h, int gw, int gh, int step, const double* __restrict__ total,
+                              int2* __restrict__ q, float* __restrict__ Z, uint8_t* __restrict__ bad) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y, pair = blockIdx.z;
+  if (x >= w) return;
+  const size_t N = static_cast<size_t>(w) * h, G = static_cast<size_t>(gw) * gh;
+  const size_t pix = static_cast<size_t>(y) * w + x;
+  double fl[6];
+  interp_exact(total + pair * G * 6, gw, gh, step, x, y, fl);
+  const double s2x = 2.0 * fl[0], s2y = 2.0 * fl[1];
+  const double nrm = __dsqrt_rn(__dadd_rn(__dmul_rn(s2x, s2x), __dmul_rn(s2y, s2y)));
+  const double z = __ddiv_rn(1.0, __dadd_rn(nrm, 1e-3));
+  Z[pair * N + pix] = __double2float_rn(z);
+  bool ok = isfinite(z);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    double wx, wy;
+    warp_pos_exact(x, y, fl, e, wx, wy);
+    const double fx = wx * 256.0, fy = wy * 256.0;
+    ok = ok && isfinite(fx) && isfinite(fy) && fabs(fx) < 1073741824.0 && fabs(fy) < 1073741824.0;
+    int2 v;
+    v.x = ok ? static_cast<int>(__double2ll_rn(fx)) : 0;
+    v.y = ok ? static_cast<int>(__double2ll_rn(fy)) : 0;
+    q[(pair * N + pix) * 4 + e] = v;
+  }
+  bad[pair * N + pix] = ok ? 0 : 1;
+}
+
+__global__ void k_occ_raster(int w, int h, const int2* __restrict__ q, const float* __restrict__ Z,
+                             const uint8_t* __restrict__ bad, unsigned long long* __restrict__ zbuf,
+                             uint8_t* __restrict__ degen) {
+  const int cw = w - 1;
+  const long long ntri = 2LL * cw * (h - 1);
+  const long long tri = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const int e = blockIdx.y, pair = blockIdx.z;
+  if (tri >= ntri) return;
+  const size_t N = static_cast<size_t>(w) * h;
+  const int t = static_cast<int>(tri & 1);
+  const int cell = static_cast<int>(tri >> 1), cx = cell % cw, cy = cell / cw;
+  const int v0 = t == 0 ? cy * w + cx : cy * w + cx + 1;
+  const int v1 = t == 0 ? cy * w + cx + 1 : (cy + 1) * w + cx + 1;
+  const int v2 = (cy + 1) * w + cx;
+  const int2* Q = q + pair * N * 4;
+  const uint8_t* B = bad + pair * N;
+  const float* ZZ = Z + pair * N;
+  const int2 p0 = Q[4 * static_cast<size_t>(v0) + e], p1 = Q[4 * static_cast<size_t>(v1) + e],
+             p2 = Q[4 * static_cast<size_t>(v2) + e];
+  const long long X[3] = {p0.x, p1.x, p2.x}, Y[3] = {p0.y, p1.y, p2.y};
+  const long long area = (X[1] - X[0]) * (Y[2] - Y[0]) - (Y[1] - Y[0]) * (X[2] - X[0]);
+  const long long mnx = min(X[0], min(X[1], X[2])), mxx = max(X[0], max(X[1], X[2]));
+  const long long mny = min(Y[0], min(Y[1], Y[2])), mxy = max(Y[0], max(Y[1], Y[2]));
+  const bool deg = B[v0] || B[v1] || B[v2] || area <= 0 || (mxx - mnx) > kZbufSpanPx * 256 ||
+                   (mxy - mny) > kZbufSpanPx * 256;
+  if (t == 0) degen[(static_cast<size_t>(pair) * 4 + e) * N + static_cast<size_t>(cy) * w + cx] = deg ? 1 : 0;
+  if (deg) return;
+  const float zf = fminf(ZZ[v0], fminf(ZZ[v1], ZZ[v2]));
+  const unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(zf)) << 32) |
+                                 static_cast<unsigned int>(tri);
+  const long long x0 = max(0LL, -((-mnx) >> 8)), x1 = min(static_cast<long long>(w - 1), mxx >> 8);
+  const long long y0 = max(0LL, -((-mny) >> 8)), y1 = min(static_cast<long long>(h - 1), mxy >> 8);
+  unsigned long long* zb = zbuf + (static_cast<size_t>(pair) * 4 + e) * N;
+  for (long long yy = y0; yy <= y1; ++yy)
+    for (long long xx = x0; xx <= x1; ++xx) {
+      const long long Px = xx * 256, Py = yy * 256;
+      bool in = true;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const int j = (i + 1) % 3;
+        const long long dx = X[j] - X[i], dy = Y[j] - Y[i];
+        const long long E = dx * (Py - Y[i]) - dy * (Px - X[i]);
+        in = in && (E > 0 || (E == 0 && (dy > 0 || (dy == 0 && dx < 0))));
+      }
+      if (in) atomicMin(zb + yy * w + xx, key);
+    }
+}
+
+__global__ void k_occ_resolve(int w, int h, const int2* __restrict__ q, const float* __restrict__ Z,
+                              const uint8_t* __restrict__ bad, const unsigned long long* __restrict__ zbuf,
+                              const uint8_t* __restrict__ degen, uint8_t* __restrict__ vis) {
+  const int px = blockIdx.x * blockDim.x + threadIdx.x, py = blockIdx.y, pair = blockIdx.z;
+  if (px >= w) return;
+  const size_t N = static_cast<size_t>(w) * h;
+  const size_t pix = static_cast<size_t>(py) * w + px;
+  const int cw = w - 1;
+  uint8_t bits = 0;
+  const bool b = bad[pair * N + pix] != 0;
+  if (w < 2 || h < 2) {
+    vis[pair * N + pix] = b ? 0 : 0x0F;
+    return;
+  }
+  const double zown = static_cast<double>(Z[pair * N + pix]);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    bool v = !b;
+    if (v && px < w - 1 && py < h - 1 && degen[(static_cast<size_t>(pair) * 4 + e) * N + pix]) v = false;
+    if (v) {
+      const int2 qq = q[(pair * N + pix) * 4 + e];
+      const long long rx = (static_cast<long long>(qq.x) + 128) >> 8, ry = (static_cast<long long>(qq.y) + 128) >> 8;
+      if (rx >= 0 && rx < w && ry >= 0 && ry < h) {
+        const unsigned long long key = zbuf[(static_cast<size_t>(pair) * 4 + e) * N + ry * w + rx];
+        if (key != ~0ULL) {
+          const unsigned int tri = static_cast<unsigned int>(key & 0xffffffffULL);
+          const int tt = tri & 1, cell = tri >> 1, ccx = cell % cw, ccy = cell / cw;
+          const bool ring = tt == 0 ? ((ccx == px && ccy == py) || (ccx == px - 1 && ccy == py) ||
+                                       (ccx == px && ccy == py - 1))
+                                    : ((ccx == px - 1 && ccy == py) || (ccx == px - 1 && ccy == py - 1) ||
+                                       (ccx == px && ccy == py - 1));
+          if (!ring) {
+            const float zf = __uint_as_float(static_cast<unsigned int>(key >> 32));
+            if (__dadd_rn(zown, -kDepthTol) > static_cast<double>(zf)) v = false;
+          }
+        }
+      }
+    }
+    if (v) bits |= static_cast<uint8_t>(1u << e);
+  }
+  vis[pair * N + pix] = bits;
+}
+
+// ---- illumination (pin C.4) ------------------------------
+__constant__ double c_gauss[32];
+__constant__ int c_gauss_r;
+
+__global__ void k_illum_resid(int w, int h, int gw, int gh, int step, const double* __restrict__ img,
+                              const double* __restrict__ total, const uint8_t* __restrict__ vis,
+                              double* __restrict__ resid) {
+  const int px = blockIdx.x * blockDim.x + threadIdx.x, py = blockIdx.y, pair = blockIdx.z;
+  if (px >= w) return;
+  const size_t N = static_cast<size_t>(w) * h, G = static_cast<size_t>(gw) * gh;
+  const size_t pix = static_cast<size_t>(py) * w + px;
+  const uint8_t v4 = vis[pair * N + pix];
+  double fl[6];
+  interp_fast(total + pair * G * 6, gw, gh, step, px, py, fl);
+  for (int t = 0; t < 2; ++t) {
+    const int e1 = 1 + 2 * t, e0 = 2 * t;
+    double r = 0.0;
+    if (((v4 >> e1) & 1) && ((v4 >> e0) & 1)) {
+      Samp s1, s0;
+      const double st = t ? 1.0 : -1.0;
+      // warp_position (c=1,t) and (c=0,t)
+      sample_img<false, false>(img + (pair * 4 + e1) * N, w, h, px + fl[0] + st * fl[2] + st * fl[4],
+                               py + fl[1] + st * fl[3] + st * fl[5], s1);
+      sample_img<false, false>(img + (pair * 4 + e0) * N, w, h, px - fl[0] + st * fl[2] - st * fl[4],
+                               py - fl[1] + st * fl[3] - st * fl[5], s0);
+      r = s1.v - s0.v;
+    }
+    resid[(pair * 2 + t) * N + pix] = r;
+  }
+}
+
+__global__ void k_blur_h(int w, int h, const double* __restrict__ src, double* __restrict__ dst) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y, plane = blockIdx.z;
+  if (x >= w) return;
+  const double* S = src + static_cast<size_t>(plane) * w * h + static_cast<size_t>(y) * w;
+  const int R = c_gauss_r;
+  double acc = 0.0;
+  for (int i = -R; i <= R; ++i) acc += c_gauss[i + R] * __ldg(S + min(max(x + i, 0), w - 1));
+  dst[static_cast<size_t>(plane) * w * h + static_cast<size_t>(y) * w + x] = acc;
+}
+
+__global__ void k_blur_v_half(int w, int h, const double* __restrict__ src, double* __restrict__ dst) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y, plane = blockIdx.z;
+  if (x >= w) return;
+  const double* S = src + static_cast<size_t>(plane) * w * h;
+  const int R = c_gauss_r;
+  double acc = 0.0;
+  for (int i = -R; i <= R; ++i) acc += c_gauss[i + R] * __ldg(S + static_cast<size_t>(min(max(y + i, 0), h - 1)) * w + x);
+  dst[static_cast<size_t>(plane) * w * h + static_cast<size_t>(y) * w + x] = 0.5 * acc;  // +-blur/2 split
+}
+
+// ---- prolongation (pins C.1/C.3/C.4) ---------------------
+__global__ void k_prolong_grid(int gwc, int ghc, int gwf, int ghf, int step, const double* __restrict__ tc,
+                               double* __restrict__ base, double* __restrict__ total, double* __restrict__ delta) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x, pair = blockIdx.y;
+  const int Gf = gwf * ghf, Gc = gwc * ghc;
+  if (k >= Gf) return;
+  const double xmax = static_cast<double>(gwc - 1) * step, ymax = static_cast<double>(ghc - 1) * step;
+  const double x = fmin(__ddiv_rn(static_cast<double>((k % gwf) * step), 2.0), xmax);
+  const double y = fmin(__ddiv_rn(static_cast<double>((k / gwf) * step), 2.0), ymax);
+  double fl[6];
+  interp_exact(tc + static_cast<size_t>(pair) * Gc * 6, gwc, ghc, step, x, y, fl);
+  const size_t o = (static_cast<size_t>(pair) * Gf + k) * 6;
+#pragma unroll
+  for (int c = 0; c < 6; ++c) {
+    const double v = 2.0 * fl[c];
+    base[o + c] = v;
+    total[o + c] = __dadd_rn(v, 0.0);
+    delta[o + c] = 0.0;
+  }
+}
+
+__global__ void k_prolong_maps(int wc, int hc, int wf, int hf, const uint8_t* __restrict__ vc,
+                               const double* __restrict__ hmc, uint8_t* __restrict__ vf, double* __restrict__ illf) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y, pair = blockIdx.z;
+  if (x >= wf) return;
+  const size_t Nc = static_cast<size_t>(wc) * hc, Nf = static_cast<size_t>(wf) * hf;
+  const size_t pix = static_cast<size_t>(y) * wf + x;
+  const uint8_t* V = vc + pair * Nc;
+  const Coord cx = cell_coord(x / 2.0, wc), cy = cell_coord(y / 2.0, hc);
+  const int x1 = min(cx.i0 + 1, wc - 1), y1 = min(cy.i0 + 1, hc - 1);
+  const uint8_t q00 = V[static_cast<size_t>(cy.i0) * wc + cx.i0], q10 = V[static_cast<size_t>(cy.i0) * wc + x1];
+  const uint8_t q01 = V[static_cast<size_t>(y1) * wc + cx.i0], q11 = V[static_cast<size_t>(y1) * wc + x1];
+  const double fx = cx.f, fy = cy.f;
+  uint8_t bits = 0;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const double v = (1 - fx) * (1 - fy) * ((q00 >> e) & 1) + fx * (1 - fy) * ((q10 >> e) & 1) +
+                     (1 - fx) * fy * ((q01 >> e) & 1) + fx * fy * ((q11 >> e) & 1);
+    if (v >= 0.5) bits |= static_cast<uint8_t>(1u << e);
+  }
+  vf[pair * Nf + pix] = bits;
+  if (hmc && illf) {
+    const size_t cpix = static_cast<size_t>(min(y / 2, hc - 1)) * wc + min(x / 2, wc - 1);
+    const double h0 = hmc[(pair * 2 + 0) * Nc + cpix], h1 = hmc[(pair * 2 + 1) * Nc + cpix];
+    illf[(pair * 4 + 0) * Nf + pix] = h0;
+    illf[(pair * 4 + 1) * Nf + pix] = -h0;
+    illf[(pair * 4 + 2) * Nf + pix] = h1;
+    illf[(pair * 4 + 3) * Nf + pix] = -h1;
+  }
+}
+
+// ---- FlowResult (geometry.hpp:26-37) via WarpGrid::interpolate ------------
+__global__ void k_dense(int w, int h, int gw, int gh, int step, const double* __restrict__ total,
+                        double* s_out, double* m_out, double* d_out, double* disp_out) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y, pair = blockIdx.z;
+  if (x >= w) return;
+  const size_t N = static_cast<size_t>(w) * h, G = static_cast<size_t>(gw) * gh;
+  const size_t pix = pair * N + static_cast<size_t>(y) * w + x;
+  double fl[6];
+  interp_exact(total + pair * G * 6, gw, gh, step, x, y, fl);
+  if (s_out) { s_out[2 * pix] = fl[0]; s_out[2 * pix + 1] = fl[1]; }
+  if (m_out) { m_out[2 * pix] = fl[2]; m_out[2 * pix + 1] = fl[3]; }
+  if (d_out) { d_out[2 * pix] = fl[4]; d_out[2 * pix + 1] = fl[5]; }
+  if (disp_out) disp_out[pix] = 2.0 * fl[0];
+}
+
+// ---- energy partials -> per (pair, slot) breakdown, fixed order -----------
+__global__ void k_energy_reduce(const double* __restrict__ ep, int nslots, int cap, int B, double* out, int* flags) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= B * nslots) return;
+  const int pair = t / nslots;
+  const double* p = ep + static_cast<size_t>(t) * cap * kNumEnergy;
+  double s[kNumEnergy] = {0, 0, 0, 0, 0};
+  for (int i = 0; i < cap; ++i)
+#pragma unroll
+    for (int k = 0; k < kNumEnergy; ++k) s[k] += p[i * kNumEnergy + k];
+  bool bad = false;
+#pragma unroll
+  for (int k = 0; k < kNumEnergy; ++k) {
+    out[static_cast<size_t>(t) * kNumEnergy + k] = s[k];
+    bad = bad || !isfinite(s[k]);
+  }
+  if (bad) atomicOr(flags + pair, kFlagEnergy);
+}
+
+inline dim3 rows_grid(int w, int h, int planes) { return dim3((w + kThreads - 1) / kThreads, h, planes); }
+
+}  // namespace
+
+void init_maps_constants() {
+  // image.cpp:127-134 with sigma = 3.2: radius ceil(3 sigma) = 10
+  const double sigma = 3.2;
+  const int R = static_cast<int>(std::ceil(3.0 * sigma));
+  double k[32];
+  double sum = 0.0;
+  for (int i = -R; i <= R; ++i) {
+    k[i + R] = std::exp(-0.5 * (i * i) / (sigma * sigma));
+    sum += k[i + R];
+  }
+  for (int i = 0; i < 2 * R + 1; ++i) k[i] /= sum;
+  cudaMemcpyToSymbol(c_gauss, k, sizeof(double) * (2 * R + 1));
+  cudaMemcpyToSymbol(c_gauss_r, &R, sizeof(int));
+}
+void launch_pyr_in(const void* src, int dtype, double* dst, long long n, cudaStream_t s) {
+  k_pyr_in<<<static_cast<unsigned>((n + kThreads - 1) / kThreads), kThreads, 0, s>>>(src, dtype, dst, n);
+}
+void launch_pyr_down(const double* src, int w, int h, double* dst, int ow, int oh, int planes, cudaStream_t s) {
+  k_pyr_down<<<rows_grid(ow, oh, planes), kThreads, 0, s>>>(src, w, h, dst, ow, oh);
+}
+void launch_init_coarse(double* base, double* total, double* delta, int G, int B, double ox, double oy,
+                        cudaStream_t s) {
+  const long long n = static_cast<long long>(G) * B;
+  k_init_coarse<<<static_cast<unsigned>((6 * n + kThreads - 1) / kThreads), kThreads, 0, s>>>(base, total, delta, n, ox, oy);
+}
+void launch_occlusion(int w, int h, int gw, int gh, int step, const double* total, int B, int2* q, float* Z,
+                      uint8_t* bad, unsigned long long* zbuf, uint8_t* degen, uint8_t* vis_out, cudaStream_t s) {
+  const size_t N = static_cast<size_t>(w) * h;
+  k_occ_project<<<rows_grid(w, h, B), kThreads, 0, s>>>(w, h, gw, gh, step, total, q, Z, bad);
+  if (w >= 2 && h >= 2) {
+    cudaMemsetAsync(zbuf, 0xFF, N * 4 * B * sizeof(unsigned long long), s);
+    const long long ntri = 2LL * (w - 1) * (h - 1);
+    k_occ_raster<<<dim3(static_cast<unsigned>((ntri + kThreads - 1) / kThreads), 4, B), kThreads, 0, s>>>(
+        w, h, q, Z, bad, zbuf, degen);
+  }
+  k_occ_resolve<<<rows_grid(w, h, B), kThreads, 0, s>>>(w, h, q, Z, bad, zbuf, degen, vis_out);
+}
+void launch_illumination(int w, int h, int gw, int gh, int step, const double* img, const double* total,
+                         const uint8_t* vis, int B, double* resid, double* tmp, double* hm, cudaStream_t s) {
+  k_illum_resid<<<rows_grid(w, h, B), kThreads, 0, s>>>(w, h, gw, gh, step, img, total, vis, resid);
+  k_blur_h<<<rows_grid(w, h, 2 * B), kThreads, 0, s>>>(w, h, resid, tmp);
+  k_blur_v_half<<<rows_grid(w, h, 2 * B), kThreads, 0, s>>>(w, h, tmp, hm);
+}
+void launch_prolong_grid(int gwc, int ghc, int gwf, int ghf, int step, const double* total_c, double* base_f,
+                         double* total_f, double* delta_f, int B, cudaStream_t s) {
+  k_prolong_grid<<<dim3((gwf * ghf + kThreads - 1) / kThreads, B), kThreads, 0, s>>>(gwc, ghc, gwf, ghf, step,
+                                                                                    total_c, base_f, total_f, delta_f);
+}
+void launch_prolong_maps(int wc, int hc, int wf, int hf, const uint8_t* vis_c, const double* hm_c, uint8_t* vis_f,
+                         double* illum_f, int B, cudaStream_t s) {
+  k_prolong_maps<<<rows_grid(wf, hf, B), kThreads, 0, s>>>(wc, hc, wf, hf, vis_c, hm_c, vis_f, illum_f);
+}
+void launch_dense(int w, int h, int gw, int gh, int step, const double* total, int B, double* s_out, double* m_out,
+                  double* d_out, double* disp_out, cudaStream_t s) {
+  k_dense<<<rows_grid(w, h, B), kThreads, 0, s>>>(w, h, gw, gh, step, total, s_out, m_out, d_out, disp_out);
+}
+void launch_energy_reduce(const double* ep, int nslots, int cap, int B, double* out, int* flags, cudaStream_t s) {
+  const int n = nslots * B;
+  k_energy_reduce<<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(ep, nslots, cap, B, out, flags);
+}
+
+}  // namespace hwf

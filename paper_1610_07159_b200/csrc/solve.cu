@@ -1,0 +1,289 @@
+// solve.cu — the inner linear solves.
+//
+// k_schwarz: one sweep of the reference's alternating-Schwarz iteration
+// (schwarz_iterate, solver.cpp:414-482): every subdomain (16 px tile of grid
+// nodes, build_subdomains solver.cpp:382-412) runs pcg_iters PCG iterations
+// (pcg_impl, solver.cpp:320-361) on its interior unknowns, warm-started from the
+// published values, with off-subdomain neighbours frozen at the previous
+// sweep's published values. One thread per local unknown; a "team" (one warp
+// for step >= 8, i.e. <= 24 unknowns) owns one subdomain; the team's rows of
+// the local matrix live in registers for the whole sweep; dots are xor-butterfly
+// warp sums (deterministic, identical in every lane). The last sweep fuses the
+// Gauss-Newton update delta += step, total = base + delta (solver.cpp:518-523).
+//
+// k_pcg_global: the subdomain_px = 0 mode (pcg_solve, solver.cpp:365-380), one
+// CTA per frame pair looping over all iterations with block-wide fixed-order dots.
+#include "launch.h"
+
+namespace hwf {
+namespace {
+
+// Row r of block(n, slot9) of the symmetric system.
+__device__ __forceinline__ double sys_entry(const double* __restrict__ sys, int G, int n, int nb,
+                                            int s9, int r, int c) {
+  if (s9 >= 4) return __ldg(sys + static_cast<size_t>(n) * kSysStride + (s9 - 4) * 21 + sym6(r, c));
+  return __ldg(sys + static_cast<size_t>(nb) * kSysStride + (4 - s9) * 21 + sym6(r, c));
+}
+
+template <int TEAM>
+__device__ __forceinline__ double team_sum(double v, double* scratch) {
+  v = warp_sum(v);
+  if (TEAM == 32) return v;
+  const int lane = threadIdx.x & 31, wt = (threadIdx.x % TEAM) >> 5;
+  __syncthreads();
+  if (lane == 0) scratch[wt] = v;
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < TEAM / 32; ++k) s += scratch[k];
+  return s;
+}
+
+template <int TEAM>
+__global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM) k_schwarz(const SwzArgs a) {
+  constexpr int SUBS = TEAM == 32 ? 4 : 1;
+  __shared__ double psh[SUBS][TEAM];
+  __shared__ double scratch[TEAM / 32 + 1];
+  const int team = threadIdx.x / TEAM, u = threadIdx.x % TEAM;
+  const int pair = blockIdx.y;
+  const int sub = blockIdx.x * SUBS + team;
+  const int G = a.gw * a.gh;
+  const bool sub_ok = sub < a.ntx * a.nty;
+  const int tx = sub_ok ? sub % a.ntx : 0, ty = sub_ok ? sub / a.ntx : 0;
+  const int alo = (tx * a.tile + a.step - 1) / a.step, ahi = min(a.gw - 1, ((tx + 1) * a.tile - 1) / a.step);
+  const int blo = (ty * a.tile + a.step - 1) / a.step, bhi = min(a.gh - 1, ((ty + 1) * a.tile - 1) / a.step);
+  const int i = u / 6, r = u % 6;
+  const int ix = i % a.nxm, iy = i / a.nxm;
+  const int na = alo + ix, nb = blo + iy;
+  const bool act = sub_ok && i < a.nxm * a.nym && na <= ahi && nb <= bhi;
+  const int n = act ? nb * a.gw + na : 0;
+  const double* sys = a.sys + static_cast<size_t>(pair) * G * kSysStride;
+  const double* pub = a.pub ? a.pub + static_cast<size_t>(pair) * G * 6 : nullptr;
+  double* psub = psh[team];
+
+  double arow[9][6];
+  int lidx[9];
+  double b = 0.0, x = 0.0;
+  if (act) {
+    b = __ldg(sys + static_cast<size_t>(n) * kSysStride + kSysRhs + r);
+    if (pub) x = __ldg(pub + 6 * static_cast<size_t>(n) + r);
+  }
+#pragma unroll
+  for (int s9 = 0; s9 < 9; ++s9) {
+    const int dx = s9 % 3 - 1, dy = s9 / 3 - 1;
+    const int qa = na + dx, qb = nb + dy;
+    const bool valid = act && qa >= 0 && qa < a.gw && qb >= 0 && qb < a.gh;
+    const bool local = valid && qa >= alo && qa <= ahi && qb >= blo && qb <= bhi;
+    const int qn = valid ? qb * a.gw + qa : 0;
+    lidx[s9] = local ? 6 * ((ix + dx) + (iy + dy) * a.nxm) : 0;
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+      const double v = valid ? sys_entry(sys, G, n, qn, s9, r, c) : 0.0;
+      arow[s9][c] = local ? v : 0.0;
+      if (valid && !local && pub) b -= v * __ldg(pub + 6 * static_cast<size_t>(qn) + c);  // solver.cpp:437-448
+    }
+  }
+  // preconditioner of this unknown's field (solver.cpp:468-474)
+  double m_self = 1.0, m_cross = 0.0;
+  if (act) {
+    const double* pre = sys + static_cast<size_t>(n) * kSysStride + kSysPre + 3 * (r >> 1);
+    m_self = __ldg(pre + ((r & 1) ? 2 : 0));
+    m_cross = __ldg(pre + 1);
+  }
+  auto apply = [&](double v) {  // local block SpMV (solver.cpp:452-467)
+    if (TEAM == 32) __syncwarp(); else __syncthreads();
+    psub[u] = v;
+    if (TEAM == 32) __syncwarp(); else __syncthreads();
+    double acc = 0.0;
+#pragma unroll
+    for (int s9 = 0; s9 < 9; ++s9)
+#pragma unroll
+      for (int c = 0; c < 6; ++c) acc += arow[s9][c] * psub[lidx[s9] + c];
+    return act ? acc : 0.0;
+  };
+  auto precond = [&](double rv) {
+    const double partner = __shfl_xor_sync(0xffffffffu, rv, 1);
+    return act ? m_self * rv + m_cross * partner : 0.0;
+  };
+
+  // pcg_impl (solver.cpp:320-361), warm start x0 = published
+  double res = b - apply(x);
+  double z = precond(res);
+  double rz = team_sum<TEAM>(res * z, scratch);
+  const double rz0 = fabs(rz);
+  int flag = 0;
+  if (rz0 != 0.0) {
+    double p = z;
+    for (int it = 0; it < a.pcg_iters; ++it) {
+      const double ap = apply(p);
+      const double pAp = team_sum<TEAM>(p * ap, scratch);
+      if (pAp <= 0.0) {
+        flag = kFlagCurvature;
+        break;
+      }
+      const double alpha = rz / pAp;
+      x += alpha * p;
+      res -= alpha * ap;
+      z = precond(res);
+      const double rzn = team_sum<TEAM>(res * z, scratch);
+      if (fabs(rzn) > 100.0 * rz0) {
+        flag = kFlagGrowth;
+        break;
+      }
+      const double beta = rzn / rz;
+      rz = rzn;
+      p = z + beta * p;
+    }
+  }
+  if (!act) return;
+  if (flag && u == 0) atomicOr(a.flags + pair, flag);
+  const size_t o = (static_cast<size_t>(pair) * G + n) * 6 + r;
+  if (a.last) {
+    if (!isfinite(x)) atomicOr(a.flags + pair, kFlagStep);
+    if ((a.active >> (r >> 1)) & 1) a.delta[o] += x;
+    a.total[o] = a.base[o] + a.delta[o];
+  } else {
+    a.next[o] = x;
+  }
+}
+
+constexpr int kPcgThreads = 1024;
+
+__device__ double block_dot(const double* __restrict__ x, const double* __restrict__ y, int n, double* red) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += x[i] * y[i];
+  s = warp_sum(s);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  double t = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+  if (threadIdx.x < 32) t = warp_sum(t);
+  __syncthreads();
+  if (threadIdx.x == 0) red[32] = t;
+  __syncthreads();
+  return red[32];
+}
+
+__device__ void spmv(const double* __restrict__ sys, int gw, int gh, const double* __restrict__ x,
+                     double* __restrict__ y) {
+  const int G = gw * gh;
+  for (int t = threadIdx.x; t < 6 * G; t += blockDim.x) {
+    const int n = t / 6, r = t % 6, na = n % gw, nb = n / gw;
+    double acc = 0.0;
+    for (int s9 = 0; s9 < 9; ++s9) {
+      const int qa = na + s9 % 3 - 1, qb = nb + s9 / 3 - 1;
+      if (qa < 0 || qa >= gw || qb < 0 || qb >= gh) continue;
+      const int qn = qb * gw + qa;
+      for (int c = 0; c < 6; ++c) acc += sys_entry(sys, G, n, qn, s9, r, c) * x[6 * qn + c];
+    }
+    y[t] = acc;
+  }
+}
+
+__device__ void precondition(const double* __restrict__ sys, int G, const double* __restrict__ r,
+                             double* __restrict__ z) {
+  for (int t = threadIdx.x; t < 6 * G; t += blockDim.x) {
+    const int n = t / 6, k = t % 6;
+    const double* pre = sys + static_cast<size_t>(n) * kSysStride + kSysPre + 3 * (k >> 1);
+    const int e = t & ~1;
+    z[t] = (k & 1) ? pre[1] * r[e] + pre[2] * r[e + 1] : pre[0] * r[e] + pre[1] * r[e + 1];
+  }
+}
+
+__global__ void __launch_bounds__(kPcgThreads) k_pcg_global(const PcgArgs a) {
+  __shared__ double red[33];
+  const int pair = blockIdx.x;
+  const int G = a.gw * a.gh, M = 6 * G;
+  const double* sys = a.sys + static_cast<size_t>(pair) * G * kSysStride;
+  double* x = a.x + static_cast<size_t>(pair) * M;
+  double* r = a.r + static_cast<size_t>(pair) * M;
+  double* z = a.z + static_cast<size_t>(pair) * M;
+  double* p = a.p + static_cast<size_t>(pair) * M;
+  double* ap = a.ap + static_cast<size_t>(pair) * M;
+  double* tr = a.trace ? a.trace + static_cast<size_t>(pair) * (a.iters + 1) : nullptr;
+  for (int t = threadIdx.x; t < M; t += blockDim.x) {
+    x[t] = 0.0;
+    r[t] = __ldg(sys + static_cast<size_t>(t / 6) * kSysStride + kSysRhs + t % 6);
+  }
+  __syncthreads();
+  if (tr) {
+    const double nr = block_dot(r, r, M, red);
+    if (threadIdx.x == 0) tr[0] = sqrt(nr);
+  }
+  precondition(sys, G, r, z);
+  __syncthreads();
+  double rz = block_dot(r, z, M, red);
+  const double rz0 = fabs(rz);
+  int flag = 0;
+  if (rz0 == 0.0) {
+    if (tr && threadIdx.x == 0)
+      for (int it = 0; it < a.iters; ++it) tr[it + 1] = 0.0;
+  } else {
+    for (int t = threadIdx.x; t < M; t += blockDim.x) p[t] = z[t];
+    __syncthreads();
+    for (int it = 0; it < a.iters; ++it) {
+      spmv(sys, a.gw, a.gh, p, ap);
+      __syncthreads();
+      const double pAp = block_dot(p, ap, M, red);
+      if (pAp <= 0.0) {
+        flag = kFlagCurvature;
+        break;
+      }
+      const double alpha = rz / pAp;
+      for (int t = threadIdx.x; t < M; t += blockDim.x) {
+        x[t] += alpha * p[t];
+        r[t] -= alpha * ap[t];
+      }
+      __syncthreads();
+      if (tr) {
+        const double nr = block_dot(r, r, M, red);
+        if (threadIdx.x == 0) tr[it + 1] = sqrt(nr);
+      }
+      precondition(sys, G, r, z);
+      __syncthreads();
+      const double rzn = block_dot(r, z, M, red);
+      if (fabs(rzn) > 100.0 * rz0) {
+        flag = kFlagGrowth;
+        break;
+      }
+      const double beta = rzn / rz;
+      rz = rzn;
+      for (int t = threadIdx.x; t < M; t += blockDim.x) p[t] = z[t] + beta * p[t];
+      __syncthreads();
+    }
+  }
+  if (flag && threadIdx.x == 0) atomicOr(a.flags + pair, flag);
+  __syncthreads();
+  if (a.update) {
+    const size_t o = static_cast<size_t>(pair) * M;
+    bool bad = false;
+    for (int t = threadIdx.x; t < M; t += blockDim.x) {
+      bad = bad || !isfinite(x[t]);
+      if ((a.active >> ((t % 6) >> 1)) & 1) a.delta[o + t] += x[t];
+      a.total[o + t] = a.base[o + t] + a.delta[o + t];
+    }
+    if (bad) atomicOr(a.flags + pair, kFlagStep);
+  }
+}
+
+}  // namespace
+
+void launch_schwarz(const SwzArgs& a, int B, cudaStream_t s) {
+  const int nsub = a.ntx * a.nty;
+  const int unknowns = 6 * a.nxm * a.nym;
+  if (unknowns <= 32) {
+    k_schwarz<32><<<dim3((nsub + 3) / 4, B), 128, 0, s>>>(a);
+  } else if (unknowns <= 128) {
+    k_schwarz<128><<<dim3(nsub, B), 128, 0, s>>>(a);
+  } else if (unknowns <= 384) {
+    k_schwarz<384><<<dim3(nsub, B), 384, 0, s>>>(a);
+  } else {
+    k_schwarz<1024><<<dim3(nsub, B), 1024, 0, s>>>(a);
+  }
+}
+
+void launch_pcg_global(const PcgArgs& a, int B, cudaStream_t s) {
+  k_pcg_global<<<B, kPcgThreads, 0, s>>>(a);
+}
+
+}  // namespace hwf

@@ -1,0 +1,96 @@
+"""Synthetic procedurally-textured stereo sequences with known flow.
+
+The reference's generator (src/synthetic.cpp) is not
+shipped; this re-creates it per SURVEY.md §8d. T(x) is seeded band-limited
+value noise (octaves at lattice spacings 4/8/16/32 px, smoothstep-bilinear) plus
+a little white noise, normalised to [0.1, 0.9]. Images are exact pull-back
+warps of T by the ground-truth flows, I_c^t(y) = T(y - sc*s - st*m - sc*st*d),
+so that I_c^t(warp_position(x, f, c, t)) = T(x) (warp_grid.hpp:73-77), then
+quantised to u8 (webcam-like).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def _octave(rng: np.random.Generator, spacing: float, xs: np.ndarray, ys: np.ndarray, extent: tuple[int, int]):
+    gx = int(np.ceil(extent[0] / spacing)) + 4
+    gy = int(np.ceil(extent[1] / spacing)) + 4
+    lat = rng.random((gy, gx))
+    u = xs / spacing + 2.0
+    v = ys / spacing + 2.0
+    i = np.clip(np.floor(u).astype(np.int64), 0, gx - 2)
+    j = np.clip(np.floor(v).astype(np.int64), 0, gy - 2)
+    fu = np.clip(u - i, 0.0, 1.0)
+    fv = np.clip(v - j, 0.0, 1.0)
+    fu = fu * fu * (3 - 2 * fu)
+    fv = fv * fv * (3 - 2 * fv)
+    a = lat[j, i] * (1 - fu) + lat[j, i + 1] * fu
+    b = lat[j + 1, i] * (1 - fu) + lat[j + 1, i + 1] * fu
+    return a * (1 - fv) + b * fv
+
+
+class Texture:
+    """Continuous, seeded texture T(x, y) over a margin-padded domain."""
+
+    def __init__(self, seed: int, w: int, h: int, margin: int = 96):
+        self.seed, self.margin = seed, margin
+        self.extent = (w + 2 * margin, h + 2 * margin)
+
+    def __call__(self, xs: np.ndarray, ys: np.ndarray) -> np.ndarray:
+        rng = np.random.default_rng(self.seed)
+        X, Y = xs + self.margin, ys + self.margin
+        t = np.zeros_like(X, dtype=np.float64)
+        for k, sp in enumerate((4.0, 8.0, 16.0, 32.0)):
+            t += (0.5 ** (3 - k)) * _octave(rng, sp, X, Y, self.extent)
+        t /= 1.875
+        return 0.1 + 0.8 * np.clip(t, 0.0, 1.0)
+
+
+def render_pair(w: int, h: int, s=(0.0, 0.0), m=(0.0, 0.0), d=(0.0, 0.0), seed: int = 1610, noise: float = 0.01,
+                occluder: dict | None = None, gain_offset: dict | None = None, dtype=np.uint8) -> np.ndarray:
+    """Four images (4, h, w) by image_index(c,t) = c + 2t for constant flows.
+
+    occluder: {"rect": (x0, y0, x1, y1) in the halfway domain, "extra_s": (sx, sy)}
+        foreground square with its own stereo flow s + extra_s (two-layer scene).
+    gain_offset: {"offset": [o0..o3], "gain": [g0..g3]} per image (illumination change).
+    """
+    T = Texture(seed, w, h)
+    Tf = Texture(seed + 7919, w, h) if occluder else None
+    yy, xx = np.mgrid[0:h, 0:w].astype(np.float64)
+    rng = np.random.default_rng(seed + 1)
+    out = np.empty((4, h, w))
+    for e in range(4):
+        sc = -1.0 if (e & 1) == 0 else 1.0
+        st = -1.0 if (e >> 1) == 0 else 1.0
+        bx = xx - sc * s[0] - st * m[0] - sc * st * d[0]
+        by = yy - sc * s[1] - st * m[1] - sc * st * d[1]
+        img = T(bx, by)
+        if occluder:
+            x0, y0, x1, y1 = occluder["rect"]
+            fs = (s[0] + occluder["extra_s"][0], s[1] + occluder["extra_s"][1])
+            fx = xx - sc * fs[0] - st * m[0] - sc * st * d[0]
+            fy = yy - sc * fs[1] - st * m[1] - sc * st * d[1]
+            inside = (fx >= x0) & (fx < x1) & (fy >= y0) & (fy < y1)
+            img = np.where(inside, Tf(fx, fy), img)
+        if gain_offset:
+            img = img * gain_offset.get("gain", [1, 1, 1, 1])[e] + gain_offset.get("offset", [0, 0, 0, 0])[e]
+        img = img + noise * rng.standard_normal(img.shape)
+        out[e] = np.clip(img, 0.0, 1.0)
+    if dtype == np.uint8:
+        return np.round(out * 255.0).astype(np.uint8)
+    return out
+
+
+def webcam_pair(index: int, w: int = 640, h: int = 480) -> tuple[np.ndarray, dict]:
+    """cfg2/cfg4 pair `index`: seed 1610+index, constant s in [0, 8] px (disparity 2s), m in [-4, 4] px."""
+    rng = np.random.default_rng(1610 + index)
+    s = (float(rng.uniform(0.0, 4.0)), 0.0)
+    m = (float(rng.uniform(-2.0, 2.0)), float(rng.uniform(-2.0, 2.0)))
+    return render_pair(w, h, s=s, m=m, seed=1610 + index), {"s": s, "m": m, "d": (0.0, 0.0)}
+
+
+def constant_pair(w: int = 320, h: int = 240, seed: int = 1610) -> tuple[np.ndarray, dict]:
+    """cfg1: s = (1.5, 0) (disparity 3 px), m = (0.75, 0.5) (motion (1.5, 1.0)), d = 0."""
+    s, m = (1.5, 0.0), (0.75, 0.5)
+    return render_pair(w, h, s=s, m=m, seed=seed), {"s": s, "m": m, "d": (0.0, 0.0)}

@@ -1,0 +1,249 @@
+"""GPU: device (libhwflow_cuda.so, sm_100a) vs the CPU oracle through the C-ABI.
+
+Tolerances (BASELINE.json north_star): pyramid and occlusion masks bit-exact;
+per-node flow within 1e-3 px max-abs after a fixed GN x PCG schedule; final
+energy within 1e-4 relative. Stage seams are checked tighter (FP64 on both
+sides, differing only in summation order): 1e-9 relative unless stated.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from paper_1610_07159_b200 import synthetic
+from paper_1610_07159_b200.hwflow import EnergyParams, LevelState, SolveSchedule, SolverDivergence, grid_dims
+
+pytestmark = pytest.mark.gpu
+
+FLOW_TOL_PX = 1e-3
+ENERGY_RTOL = 1e-4
+STAGE_RTOL = 1e-9
+
+
+def _golden_level(g, **over):
+    kw = dict(images=g["lv_images"], grid_step=int(g["lv_step"]), total=g["lv_total"], delta=g["lv_delta"],
+              vis4=g["lv_vis4"], outlier=g["lv_outlier"], node_w=g["lv_node_w"], illum=g["lv_illum"],
+              fundamental=g["lv_F"])
+    kw.update(over)
+    return LevelState(**kw)
+
+
+def _random_level(seed, w, h, step, illum=True):
+    rng = np.random.default_rng(seed)
+    imgs = synthetic.render_pair(w, h, s=(1.0, 0.3), m=(0.4, -0.6), seed=seed, dtype=np.float64)
+    gw, gh = grid_dims(w, h, step)
+    return LevelState(imgs, step, rng.normal(0, 0.7, (gw * gh, 6)), rng.normal(0, 0.2, (gw * gh, 6)),
+                      rng.integers(0, 16, (h, w)).astype(np.uint8), (rng.random((h, w)) > 0.15).astype(np.uint8),
+                      rng.uniform(1, 100, gw * gh), rng.normal(0, 0.02, (4, h, w)) if illum else None,
+                      np.array([[0, 0, 0], [0, 0, -1], [0, 1, 0.0]]))
+
+
+# ---- pyramid: bit-exact -------------------------------------------------------------
+def test_pyramid_bit_exact(device, oracle, golden):
+    for l, lev in enumerate(device.build_pyramid(golden["pyr_in"], 4)):
+        assert np.array_equal(lev, golden[f"pyr_L{l}"]), l
+    rng = np.random.default_rng(3)
+    for shape in ((4, 480, 640), (4, 37, 53), (4, 1, 9)):
+        im = rng.integers(0, 256, shape).astype(np.uint8)
+        for a, b in zip(device.build_pyramid(im, 4), oracle.build_pyramid(im, 4)):
+            assert np.array_equal(a, b)
+    f = rng.normal(0.5, 0.4, (4, 31, 17))  # F64 input: clamped to [0,1]
+    for a, b in zip(device.build_pyramid(f, 3), oracle.build_pyramid(f, 3)):
+        assert np.array_equal(a, b)
+
+
+# ---- energy / weights / linearization ------------------------------------------------
+@pytest.mark.parametrize("preset", ["live", "facial", "stereo-hq"])
+def test_energy_matches_oracle(device, oracle, golden, preset):
+    P = EnergyParams.preset(preset)
+    for lv in (_golden_level(golden), _random_level(2, 70, 45, 8), _random_level(4, 33, 29, 2, illum=False)):
+        a, _ = device.energy(lv, P)
+        b, _ = oracle.energy(lv, P)
+        for k in ("photo", "grad", "smooth", "epi", "mag", "total"):
+            assert getattr(a, k) == pytest.approx(getattr(b, k), rel=STAGE_RTOL, abs=1e-12), k
+        assert a.residual_count == b.residual_count
+
+
+def test_refresh_weights_match_oracle(device, oracle, golden):
+    for lv in (_golden_level(golden), _random_level(5, 64, 40, 8), _random_level(6, 35, 21, 4)):
+        for P in (EnergyParams(), EnergyParams.preset("facial")):
+            Wa, na = device.refresh_weights(lv, P)
+            Wb, nb = oracle.refresh_weights(lv, P)
+            assert np.array_equal(Wa, Wb)
+            np.testing.assert_allclose(na, nb, rtol=1e-9)
+
+
+@pytest.mark.parametrize("active,lm", [(7, 0.0), (1, 0.0), (5, 0.3)])
+def test_linearize_matches_oracle(device, oracle, golden, active, lm):
+    for lv in (_golden_level(golden), _random_level(8, 50, 34, 8), _random_level(9, 27, 19, 2)):
+        for P in (EnergyParams(), EnergyParams.preset("stereo-hq")):
+            ba, ra, pa = device.build_normal_system(lv, P, active, lm)
+            bb, rb, pb = oracle.build_normal_system(lv, P, active, lm)
+            np.testing.assert_allclose(ba, bb, rtol=0, atol=STAGE_RTOL * np.abs(bb).max())
+            np.testing.assert_allclose(ra, rb, rtol=0, atol=STAGE_RTOL * np.abs(rb).max())
+            np.testing.assert_allclose(pa, pb, rtol=1e-7, atol=1e-12 * np.abs(pb).max())
+
+
+def test_pcg_and_schwarz_match_reference_golden(device, golden):
+    gw, gh = grid_dims(24, 20, 4)
+    x, tr = device.pcg_solve(gw, gh, golden["blocks_live"], golden["rhs_live"], 10, trace=True)
+    np.testing.assert_allclose(x, golden["pcg_x"], rtol=0, atol=1e-9 * np.abs(golden["pcg_x"]).max())
+    np.testing.assert_allclose(tr, golden["pcg_trace"], rtol=1e-8)
+    xs = device.schwarz_iterate(gw, gh, 4, golden["blocks_live"], golden["rhs_live"], 3, 4)
+    np.testing.assert_allclose(xs, golden["schwarz_x"], rtol=0, atol=1e-9 * np.abs(golden["schwarz_x"]).max())
+
+
+def test_schwarz_step8_and_global_match_oracle(device, oracle):
+    lv = _random_level(12, 96, 64, 8)
+    b, r, _ = oracle.build_normal_system(lv, EnergyParams())
+    gw, gh = grid_dims(96, 64, 8)
+    for pi, ki in ((1, 5), (5, 5), (3, 10)):
+        xa = device.schwarz_iterate(gw, gh, 8, b, r, pi, ki)
+        xb = oracle.schwarz_iterate(gw, gh, 8, b, r, pi, ki)
+        np.testing.assert_allclose(xa, xb, rtol=0, atol=1e-9 * np.abs(xb).max())
+    xa = device.pcg_solve(gw, gh, b, r, 25)
+    xb = oracle.pcg_solve(gw, gh, b, r, 25)
+    np.testing.assert_allclose(xa, xb, rtol=0, atol=1e-9 * np.abs(xb).max())
+
+
+@pytest.mark.parametrize("mode,sub", [("schwarz", 16), ("global", 0)])
+def test_gauss_newton_level_matches_reference_golden(device, golden, mode, sub):
+    gw, gh = grid_dims(40, 32, 8)
+    lv = LevelState(golden["gn_images"], 8, np.zeros((gw * gh, 6)), np.zeros((gw * gh, 6)))
+    S = SolveSchedule(levels=1, grid_step=8, pcg_iters=5, patch_iters=5, subdomain_px=sub)
+    d, W, nw, eb, ea = device.gauss_newton(lv, np.zeros((gw * gh, 6)), EnergyParams(), S, 3)
+    assert np.abs(d - golden[f"gn_{mode}_delta"]).max() < FLOW_TOL_PX
+    assert np.array_equal(W, golden[f"gn_{mode}_W"])
+    np.testing.assert_allclose(eb, golden[f"gn_{mode}_eb"], rtol=ENERGY_RTOL)
+    np.testing.assert_allclose(ea, golden[f"gn_{mode}_ea"], rtol=ENERGY_RTOL)
+
+
+# ---- occlusion (bit-exact on identical input flows), illumination, prolongation --------
+def _wavy_total(seed, w, h, step, amp):
+    rng = np.random.default_rng(seed)
+    gw, gh = grid_dims(w, h, step)
+    t = rng.normal(0, amp, (gw * gh, 6))
+    t[:, 0] += 3.0
+    return t
+
+
+def test_occlusion_bit_exact(device, oracle):
+    for seed, (w, h, step, amp) in enumerate(((64, 48, 8, 0.8), (100, 61, 4, 1.5), (33, 17, 2, 0.6), (640, 480, 8, 2.0))):
+        t = _wavy_total(seed, w, h, step, amp)
+        va = device.compute_occlusion_maps(w, h, step, t)
+        vb = oracle.compute_occlusion_maps(w, h, step, t)
+        assert np.array_equal(va, vb)
+        assert (va != 0x0F).any()  # the case actually occludes something
+    gw, gh = grid_dims(21, 13, 4)
+    assert np.all(device.compute_occlusion_maps(21, 13, 4, np.zeros((gw * gh, 6))) == 0x0F)
+
+
+def test_occlusion_two_layer_scene(device, oracle):
+    # foreground band with larger disparity: background beside it is occluded in one camera
+    w, h, step = 96, 64, 4
+    gw, gh = grid_dims(w, h, step)
+    t = np.zeros((gw * gh, 6))
+    t[:, 0] = 1.0
+    a = np.arange(gw * gh) % gw
+    t[(a >= 10) & (a <= 14), 0] = 5.0
+    va, vb = device.compute_occlusion_maps(w, h, step, t), oracle.compute_occlusion_maps(w, h, step, t)
+    assert np.array_equal(va, vb)
+    assert ((va & 0b0101) != 0b0101).any() or ((va & 0b1010) != 0b1010).any()
+
+
+def test_illumination_matches_oracle(device, oracle):
+    lv = _random_level(21, 80, 60, 8)
+    vis = oracle.compute_occlusion_maps(80, 60, 8, lv.total)
+    ha = device.compute_illumination_maps(lv.images, 8, lv.total, vis)
+    hb = oracle.compute_illumination_maps(lv.images, 8, lv.total, vis)
+    np.testing.assert_allclose(ha, hb, rtol=0, atol=1e-12)
+
+
+def test_prolongation_bit_exact(device, oracle):
+    rng = np.random.default_rng(2)
+    for (wc, hc, wf, hf, step) in ((40, 30, 80, 60, 8), (21, 11, 41, 21, 4), (160, 120, 320, 240, 8)):
+        gwc, ghc = grid_dims(wc, hc, step)
+        tc = rng.normal(0, 2, (gwc * ghc, 6))
+        vc = rng.integers(0, 16, (hc, wc)).astype(np.uint8)
+        hm = rng.normal(0, 0.1, (2, hc, wc))
+        a = device.prolongate(wc, hc, wf, hf, step, tc, vc, hm)
+        b = oracle.prolongate(wc, hc, wf, hf, step, tc, vc, hm)
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
+
+
+# ---- Algorithm 1 end to end -------------------------------------------------------
+def _check_solve(device, oracle, imgs, P, S, F=None):
+    (ra,), (sa,) = device.solve_batch(imgs[None], P, S, F)
+    rb, sb = oracle.run_scene_flow(imgs, P, S, F)
+    assert np.abs(ra.grid_total - rb.grid_total).max() < FLOW_TOL_PX
+    assert np.abs(ra.disparity - rb.disparity).max() < 2 * FLOW_TOL_PX
+    for l in range(len(sb.energy_after)):
+        np.testing.assert_allclose(sa.energy_before[l], sb.energy_before[l], rtol=ENERGY_RTOL)
+        np.testing.assert_allclose(sa.energy_after[l], sb.energy_after[l], rtol=ENERGY_RTOL)
+    agree = (ra.vis4 == rb.vis4).mean()
+    assert agree > 0.999, agree  # masks bit-exact on identical flows; flows differ by <1e-3 px here
+    return ra, sa
+
+
+def test_solve_cfg1_global_pcg(device, oracle):
+    imgs, gt = synthetic.constant_pair(320, 240)
+    S = SolveSchedule(levels=3, grid_step=8, gn_per_level=[5], pcg_iters=10, subdomain_px=0)
+    r, s = _check_solve(device, oracle, imgs, EnergyParams(), S)
+    assert abs(np.median(r.s[..., 0]) - gt["s"][0]) < 0.25
+
+
+def test_solve_short_schwarz_schedule(device, oracle):
+    imgs, _ = synthetic.webcam_pair(3, 160, 120)
+    S = SolveSchedule(levels=3, grid_step=8, gn_per_level=[1, 1, 2], pcg_iters=5, patch_iters=5, subdomain_px=16)
+    _check_solve(device, oracle, imgs, EnergyParams(), S)
+
+
+def test_solve_epipolar_and_stereo_only(device, oracle):
+    imgs, _ = synthetic.constant_pair(96, 64)
+    F = np.array([[0, 0, 0], [0, 0, -1], [0, 1, 0.0]])
+    S = SolveSchedule(levels=2, grid_step=4, gn_per_level=[2], pcg_iters=6, subdomain_px=0, lm_lambda=0.1)
+    _check_solve(device, oracle, imgs, EnergyParams.preset("facial"), S, F)
+    S1 = SolveSchedule(levels=2, grid_step=8, gn_per_level=[2], pcg_iters=6, subdomain_px=0, active_fields=1,
+                       coarse_s_offset=(0.5, 0.0))
+    r, _ = _check_solve(device, oracle, imgs, EnergyParams(), S1)
+    assert np.abs(r.grid_total[:, 2:]).max() == 0.0  # m, d pinned (solver.cpp:218-220)
+
+
+def test_batch_is_bitwise_independent(device):
+    frames = np.stack([synthetic.webcam_pair(i, 128, 96)[0] for i in range(3)])
+    S = SolveSchedule(levels=3, grid_step=8, pcg_iters=5, patch_iters=5)
+    batch, _ = device.solve_batch(frames, EnergyParams(), S)
+    for i in range(3):
+        (single,), _ = device.solve_batch(frames[i:i + 1], EnergyParams(), S)
+        assert np.array_equal(single.grid_total, batch[i].grid_total)
+        assert np.array_equal(single.vis4, batch[i].vis4)
+    again, _ = device.solve_batch(frames, EnergyParams(), S)
+    assert all(np.array_equal(a.grid_total, b.grid_total) for a, b in zip(batch, again))
+
+
+def test_cfg2_full_size_properties(device):
+    """BASELINE cfg2 shape on a batch: finite, deterministic, identity scene stationary."""
+    frames = np.stack([synthetic.webcam_pair(i)[0] for i in range(4)])
+    S = SolveSchedule(levels=4, grid_step=8, pcg_iters=5, patch_iters=5, subdomain_px=16)
+    res, st = device.solve_batch(frames, EnergyParams(), S, outputs=("grid_total", "vis4"))
+    for r, s in zip(res, st):
+        assert np.isfinite(r.grid_total).all()
+        assert len(s.energy_after) == 4 and [len(e) for e in s.energy_after] == [2, 2, 5, 5]
+    ident = np.stack([np.repeat(frames[0, :1], 4, axis=0)])  # four identical images
+    (r,), (s,) = device.solve_batch(ident, EnergyParams(), SolveSchedule(levels=4, grid_step=8, subdomain_px=0))
+    assert np.abs(r.grid_total).max() < 1e-6  # SPEC.md:348 stationarity
+    assert np.all(r.vis4 == 0x0F)
+
+
+def test_divergence_is_reported(device):
+    imgs, _ = synthetic.constant_pair(64, 48)
+    P = EnergyParams(m_s=0.0, m_m=0.0, m_d=0.0, w_reg=0.0)  # no Tikhonov: J^T J singular on flat regions
+    imgs = np.zeros_like(imgs)
+    S = SolveSchedule(levels=1, grid_step=8, gn_per_level=[1], pcg_iters=5, subdomain_px=0)
+    try:
+        device.solve_batch(imgs[None], P, S)
+    except SolverDivergence:
+        pass  # reported, not aborted
+    with pytest.raises(ValueError):
+        device.solve_batch(imgs[None], EnergyParams.preset("facial"), S)  # w_epi > 0 without F
