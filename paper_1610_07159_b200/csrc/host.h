@@ -121,6 +121,8 @@ struct Scratch {  // shared across levels, sized for the finest
   uint8_t* bad = nullptr;
   unsigned long long* zbuf = nullptr;
   uint8_t* degen = nullptr;
+  unsigned long long* queue = nullptr;  // large-triangle raster queue (every triangle, worst case)
+  unsigned int* qcount = nullptr;
   double *resid = nullptr, *tmp = nullptr;
   double *px = nullptr, *pr = nullptr, *pz = nullptr, *pp = nullptr, *pap = nullptr;
   void alloc(DevMem& m, int B, size_t N, size_t G, bool occ, bool illum, bool pcg) {
@@ -130,6 +132,8 @@ struct Scratch {  // shared across levels, sized for the finest
       bad = m.alloc<uint8_t>(B * N);
       zbuf = m.alloc<unsigned long long>(B * N * 4);
       degen = m.alloc<uint8_t>(B * N * 4);
+      queue = m.alloc<unsigned long long>(B * N * 8);
+      qcount = m.alloc<unsigned int>(1);
     }
     if (illum) {
       resid = m.alloc<double>(B * N * 2);
@@ -359,8 +363,9 @@ struct Plan {
       CK(cudaMemsetAsync(d.W, 1, B * d.N, st));
       CK(cudaMemsetAsync(d.nodew, 0, sizeof(double) * B * d.G, st));
       record_gn_level(d, B, P, S, dF, gn[l], E, slot_base[l], sc, flags, st, LC);
-      launch_occlusion(d.w, d.h, d.gw, d.gh, d.step, d.total, B, sc.q, sc.Z, sc.bad, sc.zbuf, sc.degen, d.occ, st);
-      LC.count += 3;
+      launch_occlusion(d.w, d.h, d.gw, d.gh, d.step, d.total, B, sc.q, sc.Z, sc.bad, sc.zbuf, sc.degen, sc.queue,
+                       sc.qcount, d.occ, st);
+      LC.count += 4;
       if (l > 0) {
         launch_illumination(d.w, d.h, d.gw, d.gh, d.step, d.img, d.total, d.occ, B, sc.resid, sc.tmp, d.hm, st);
         LC.count += 3;

@@ -107,7 +107,7 @@ void launch_init_coarse(double* base, double* total, double* delta, int G, int B
                         double oy, cudaStream_t s);
 void launch_occlusion(int w, int h, int gw, int gh, int step, const double* total, int B,
                       int2* q, float* Z, uint8_t* bad, unsigned long long* zbuf, uint8_t* degen,
-                      uint8_t* vis_out, cudaStream_t s);
+                      unsigned long long* queue, unsigned int* qcount, uint8_t* vis_out, cudaStream_t s);
 void launch_illumination(int w, int h, int gw, int gh, int step, const double* img,
                          const double* total, const uint8_t* vis, int B, double* resid,
                          double* tmp, double* hm, cudaStream_t s);

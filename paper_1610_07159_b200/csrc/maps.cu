@@ -84,52 +84,116 @@ __global__ void k_occ_project(int w, int h, int gw, int gh, int step, const doub
   bad[pair * N + pix] = ok ? 0 : 1;
 }
 
+struct Tri {
+  long long X[3], Y[3];
+  long long mnx, mxx, mny, mxy;
+};
+
+// Vertices of triangle `tri` of the halfway lattice in view e (pin C.2).
+__device__ __forceinline__ void tri_vertices(int w, long long tri, int& v0, int& v1, int& v2) {
+  const int cw = w - 1, t = static_cast<int>(tri & 1);
+  const int cell = static_cast<int>(tri >> 1), cx = cell % cw, cy = cell / cw;
+  v0 = t == 0 ? cy * w + cx : cy * w + cx + 1;
+  v1 = t == 0 ? cy * w + cx + 1 : (cy + 1) * w + cx + 1;
+  v2 = (cy + 1) * w + cx;
+}
+
+__device__ __forceinline__ void load_tri(const int2* __restrict__ Q, int e, int v0, int v1, int v2, Tri& T) {
+  const int2 p0 = Q[4 * static_cast<size_t>(v0) + e], p1 = Q[4 * static_cast<size_t>(v1) + e],
+             p2 = Q[4 * static_cast<size_t>(v2) + e];
+  T.X[0] = p0.x; T.X[1] = p1.x; T.X[2] = p2.x;
+  T.Y[0] = p0.y; T.Y[1] = p1.y; T.Y[2] = p2.y;
+  T.mnx = min(T.X[0], min(T.X[1], T.X[2]));
+  T.mxx = max(T.X[0], max(T.X[1], T.X[2]));
+  T.mny = min(T.Y[0], min(T.Y[1], T.Y[2]));
+  T.mxy = max(T.Y[0], max(T.Y[1], T.Y[2]));
+}
+
+// int64 edge functions with the top-left tie rule (pin C.2)
+__device__ __forceinline__ bool covers(const Tri& T, long long Px, long long Py) {
+  bool in = true;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const int j = (i + 1) % 3;
+    const long long dx = T.X[j] - T.X[i], dy = T.Y[j] - T.Y[i];
+    const long long E = dx * (Py - T.Y[i]) - dy * (Px - T.X[i]);
+    in = in && (E > 0 || (E == 0 && (dy > 0 || (dy == 0 && dx < 0))));
+  }
+  return in;
+}
+
+constexpr int kSmallBoxPx = 16;  // triangles whose pixel box exceeds this go to the warp queue
+
+// One thread per (triangle, view, pair). Degeneracy test, flat depth key,
+// small boxes rasterised in-thread; large boxes queued for k_occ_raster_big.
+// atomicMin on (depth bits, triangle id) makes the z-buffer order-independent.
 __global__ void k_occ_raster(int w, int h, const int2* __restrict__ q, const float* __restrict__ Z,
                              const uint8_t* __restrict__ bad, unsigned long long* __restrict__ zbuf,
-                             uint8_t* __restrict__ degen) {
-  const int cw = w - 1;
-  const long long ntri = 2LL * cw * (h - 1);
+                             uint8_t* __restrict__ degen, unsigned long long* __restrict__ queue,
+                             unsigned int* __restrict__ qcount) {
+  const long long ntri = 2LL * (w - 1) * (h - 1);
   const long long tri = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   const int e = blockIdx.y, pair = blockIdx.z;
   if (tri >= ntri) return;
   const size_t N = static_cast<size_t>(w) * h;
-  const int t = static_cast<int>(tri & 1);
-  const int cell = static_cast<int>(tri >> 1), cx = cell % cw, cy = cell / cw;
-  const int v0 = t == 0 ? cy * w + cx : cy * w + cx + 1;
-  const int v1 = t == 0 ? cy * w + cx + 1 : (cy + 1) * w + cx + 1;
-  const int v2 = (cy + 1) * w + cx;
-  const int2* Q = q + pair * N * 4;
+  int v0, v1, v2;
+  tri_vertices(w, tri, v0, v1, v2);
   const uint8_t* B = bad + pair * N;
-  const float* ZZ = Z + pair * N;
-  const int2 p0 = Q[4 * static_cast<size_t>(v0) + e], p1 = Q[4 * static_cast<size_t>(v1) + e],
-             p2 = Q[4 * static_cast<size_t>(v2) + e];
-  const long long X[3] = {p0.x, p1.x, p2.x}, Y[3] = {p0.y, p1.y, p2.y};
-  const long long area = (X[1] - X[0]) * (Y[2] - Y[0]) - (Y[1] - Y[0]) * (X[2] - X[0]);
-  const long long mnx = min(X[0], min(X[1], X[2])), mxx = max(X[0], max(X[1], X[2]));
-  const long long mny = min(Y[0], min(Y[1], Y[2])), mxy = max(Y[0], max(Y[1], Y[2]));
-  const bool deg = B[v0] || B[v1] || B[v2] || area <= 0 || (mxx - mnx) > kZbufSpanPx * 256 ||
-                   (mxy - mny) > kZbufSpanPx * 256;
-  if (t == 0) degen[(static_cast<size_t>(pair) * 4 + e) * N + static_cast<size_t>(cy) * w + cx] = deg ? 1 : 0;
+  Tri T;
+  load_tri(q + pair * N * 4, e, v0, v1, v2, T);
+  const long long area = (T.X[1] - T.X[0]) * (T.Y[2] - T.Y[0]) - (T.Y[1] - T.Y[0]) * (T.X[2] - T.X[0]);
+  const bool deg = B[v0] || B[v1] || B[v2] || area <= 0 || (T.mxx - T.mnx) > kZbufSpanPx * 256 ||
+                   (T.mxy - T.mny) > kZbufSpanPx * 256;
+  if ((tri & 1) == 0) degen[(static_cast<size_t>(pair) * 4 + e) * N + v0] = deg ? 1 : 0;
   if (deg) return;
+  const long long x0 = max(0LL, -((-T.mnx) >> 8)), x1 = min(static_cast<long long>(w - 1), T.mxx >> 8);
+  const long long y0 = max(0LL, -((-T.mny) >> 8)), y1 = min(static_cast<long long>(h - 1), T.mxy >> 8);
+  if (x1 < x0 || y1 < y0) return;
+  if ((x1 - x0 + 1) * (y1 - y0 + 1) > kSmallBoxPx) {
+    const unsigned int slot = atomicAdd(qcount, 1u);
+    queue[slot] = (static_cast<unsigned long long>(pair) << 34) | (static_cast<unsigned long long>(e) << 32) |
+                  static_cast<unsigned long long>(tri);
+    return;
+  }
+  const float* ZZ = Z + pair * N;
   const float zf = fminf(ZZ[v0], fminf(ZZ[v1], ZZ[v2]));
   const unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(zf)) << 32) |
                                  static_cast<unsigned int>(tri);
-  const long long x0 = max(0LL, -((-mnx) >> 8)), x1 = min(static_cast<long long>(w - 1), mxx >> 8);
-  const long long y0 = max(0LL, -((-mny) >> 8)), y1 = min(static_cast<long long>(h - 1), mxy >> 8);
   unsigned long long* zb = zbuf + (static_cast<size_t>(pair) * 4 + e) * N;
   for (long long yy = y0; yy <= y1; ++yy)
-    for (long long xx = x0; xx <= x1; ++xx) {
-      const long long Px = xx * 256, Py = yy * 256;
-      bool in = true;
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        const int j = (i + 1) % 3;
-        const long long dx = X[j] - X[i], dy = Y[j] - Y[i];
-        const long long E = dx * (Py - Y[i]) - dy * (Px - X[i]);
-        in = in && (E > 0 || (E == 0 && (dy > 0 || (dy == 0 && dx < 0))));
-      }
-      if (in) atomicMin(zb + yy * w + xx, key);
+    for (long long xx = x0; xx <= x1; ++xx)
+      if (covers(T, xx * 256, yy * 256)) atomicMin(zb + yy * w + xx, key);
+}
+
+// Warp per queued large triangle; lanes stride over its pixel box.
+__global__ void k_occ_raster_big(int w, int h, const int2* __restrict__ q, const float* __restrict__ Z,
+                                 unsigned long long* __restrict__ zbuf, const unsigned long long* __restrict__ queue,
+                                 const unsigned int* __restrict__ qcount) {
+  const int lane = threadIdx.x & 31;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarp = (gridDim.x * blockDim.x) >> 5;
+  const unsigned int n = *qcount;
+  const size_t N = static_cast<size_t>(w) * h;
+  for (unsigned int i = gwarp; i < n; i += nwarp) {
+    const unsigned long long item = queue[i];
+    const int pair = static_cast<int>(item >> 34), e = static_cast<int>((item >> 32) & 3);
+    const long long tri = static_cast<long long>(item & 0xffffffffULL);
+    int v0, v1, v2;
+    tri_vertices(w, tri, v0, v1, v2);
+    Tri T;
+    load_tri(q + pair * N * 4, e, v0, v1, v2, T);
+    const float* ZZ = Z + pair * N;
+    const float zf = fminf(ZZ[v0], fminf(ZZ[v1], ZZ[v2]));
+    const unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(zf)) << 32) |
+                                   static_cast<unsigned int>(tri);
+    const long long x0 = max(0LL, -((-T.mnx) >> 8)), x1 = min(static_cast<long long>(w - 1), T.mxx >> 8);
+    const long long y0 = max(0LL, -((-T.mny) >> 8)), y1 = min(static_cast<long long>(h - 1), T.mxy >> 8);
+    const long long bw = x1 - x0 + 1, nb = bw * (y1 - y0 + 1);
+    unsigned long long* zb = zbuf + (static_cast<size_t>(pair) * 4 + e) * N;
+    for (long long k = lane; k < nb; k += 32) {
+      const long long xx = x0 + k % bw, yy = y0 + k / bw;
+      if (covers(T, xx * 256, yy * 256)) atomicMin(zb + yy * w + xx, key);
     }
+  }
 }
 
 __global__ void k_occ_resolve(int w, int h, const int2* __restrict__ q, const float* __restrict__ Z,
@@ -293,22 +357,28 @@ __global__ void k_dense(int w, int h, int gw, int gh, int step, const double* __
 }
 
 // ---- energy partials -> per (pair, slot) breakdown, fixed order -----------
+// Warp per (pair, slot): lane l sums partials l, l+32, ... in order, then a
+// fixed xor tree — deterministic and independent of scheduling.
 __global__ void k_energy_reduce(const double* __restrict__ ep, int nslots, int cap, int B, double* out, int* flags) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (t >= B * nslots) return;
   const int pair = t / nslots;
   const double* p = ep + static_cast<size_t>(t) * cap * kNumEnergy;
   double s[kNumEnergy] = {0, 0, 0, 0, 0};
-  for (int i = 0; i < cap; ++i)
+  for (int i = lane; i < cap; i += 32)
 #pragma unroll
     for (int k = 0; k < kNumEnergy; ++k) s[k] += p[i * kNumEnergy + k];
   bool bad = false;
 #pragma unroll
   for (int k = 0; k < kNumEnergy; ++k) {
-    out[static_cast<size_t>(t) * kNumEnergy + k] = s[k];
+    s[k] = warp_sum(s[k]);
     bad = bad || !isfinite(s[k]);
   }
-  if (bad) atomicOr(flags + pair, kFlagEnergy);
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < kNumEnergy; ++k) out[static_cast<size_t>(t) * kNumEnergy + k] = s[k];
+    if (bad) atomicOr(flags + pair, kFlagEnergy);
+  }
 }
 
 inline dim3 rows_grid(int w, int h, int planes) { return dim3((w + kThreads - 1) / kThreads, h, planes); }
@@ -341,14 +411,17 @@ void launch_init_coarse(double* base, double* total, double* delta, int G, int B
   k_init_coarse<<<static_cast<unsigned>((6 * n + kThreads - 1) / kThreads), kThreads, 0, s>>>(base, total, delta, n, ox, oy);
 }
 void launch_occlusion(int w, int h, int gw, int gh, int step, const double* total, int B, int2* q, float* Z,
-                      uint8_t* bad, unsigned long long* zbuf, uint8_t* degen, uint8_t* vis_out, cudaStream_t s) {
+                      uint8_t* bad, unsigned long long* zbuf, uint8_t* degen, unsigned long long* queue,
+                      unsigned int* qcount, uint8_t* vis_out, cudaStream_t s) {
   const size_t N = static_cast<size_t>(w) * h;
   k_occ_project<<<rows_grid(w, h, B), kThreads, 0, s>>>(w, h, gw, gh, step, total, q, Z, bad);
   if (w >= 2 && h >= 2) {
     cudaMemsetAsync(zbuf, 0xFF, N * 4 * B * sizeof(unsigned long long), s);
+    cudaMemsetAsync(qcount, 0, sizeof(unsigned int), s);
     const long long ntri = 2LL * (w - 1) * (h - 1);
     k_occ_raster<<<dim3(static_cast<unsigned>((ntri + kThreads - 1) / kThreads), 4, B), kThreads, 0, s>>>(
-        w, h, q, Z, bad, zbuf, degen);
+        w, h, q, Z, bad, zbuf, degen, queue, qcount);
+    k_occ_raster_big<<<148 * 8, kThreads, 0, s>>>(w, h, q, Z, zbuf, queue, qcount);
   }
   k_occ_resolve<<<rows_grid(w, h, B), kThreads, 0, s>>>(w, h, q, Z, bad, zbuf, degen, vis_out);
 }
@@ -372,8 +445,8 @@ void launch_dense(int w, int h, int gw, int gh, int step, const double* total, i
   k_dense<<<rows_grid(w, h, B), kThreads, 0, s>>>(w, h, gw, gh, step, total, s_out, m_out, d_out, disp_out);
 }
 void launch_energy_reduce(const double* ep, int nslots, int cap, int B, double* out, int* flags, cudaStream_t s) {
-  const int n = nslots * B;
-  k_energy_reduce<<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(ep, nslots, cap, B, out, flags);
+  const long long n = 32LL * nslots * B;
+  k_energy_reduce<<<static_cast<unsigned>((n + kThreads - 1) / kThreads), kThreads, 0, s>>>(ep, nslots, cap, B, out, flags);
 }
 
 }  // namespace hwf

@@ -387,7 +387,8 @@ int hwf_occlusion(hwf_ctx* ctx, int w, int h, int step, const double* total, uin
     Scratch sc;
     sc.alloc(m, 1, d.N, d.G, true, false, false);
     uint8_t* vis = m.alloc<uint8_t>(d.N);
-    launch_occlusion(w, h, d.gw, d.gh, step, dt, 1, sc.q, sc.Z, sc.bad, sc.zbuf, sc.degen, vis, ctx->stream);
+    launch_occlusion(w, h, d.gw, d.gh, step, dt, 1, sc.q, sc.Z, sc.bad, sc.zbuf, sc.degen, sc.queue, sc.qcount, vis,
+                     ctx->stream);
     CK(cudaStreamSynchronize(ctx->stream));
     CK(cudaGetLastError());
     down(vis4_out, vis, d.N);

@@ -80,6 +80,19 @@ def main() -> None:
         d, W, nw, eb, ea = ref.gauss_newton(lv2, np.zeros((gw * gh, 6)), EnergyParams(), S, 3)
         out[f"gn_{mode}_delta"], out[f"gn_{mode}_W"], out[f"gn_{mode}_nw"] = d, W, nw
         out[f"gn_{mode}_eb"], out[f"gn_{mode}_ea"] = eb, ea
+    # full cfg1 solves (Algorithm 1 with the reference's own gauss_newton), for the
+    # end-to-end reproducibility bar: the reference is ill-conditioned on the full
+    # schedule, so its own build and the oracle port differ by ~1e-2 px there.
+    port = Solver(ROOT / "oracle" / "_build" / "libhwflow_oracle.so")
+    imgs, _ = synthetic.constant_pair(320, 240)
+    out["cfg1_images"] = imgs
+    for tag, gl in (("full", [5]), ("short", [5, 5, 3])):
+        S = SolveSchedule(levels=3, grid_step=8, gn_per_level=gl, pcg_iters=10, subdomain_px=0)
+        r, st = ref.run_scene_flow(imgs, EnergyParams(), S)
+        q, _ = port.run_scene_flow(imgs, EnergyParams(), S)
+        out[f"cfg1_{tag}_grid"], out[f"cfg1_{tag}_vis4"] = r.grid_total, r.vis4
+        out[f"cfg1_{tag}_E"] = np.array(st.final_energy())
+        out[f"cfg1_{tag}_port_vs_ref"] = np.array(np.abs(q.grid_total - r.grid_total).max())
     path = ROOT / "tests" / "golden" / "ref_small.npz"
     np.savez_compressed(path, **out)
     print(f"wrote {path} ({path.stat().st_size} bytes, {len(out)} arrays)")
