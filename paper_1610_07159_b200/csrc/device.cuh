@@ -158,6 +158,39 @@ __device__ __forceinline__ void sample_img(const double* __restrict__ I, int w, 
   }
 }
 
+// Bilinear footprint of a continuous position (image.cpp:19-31,37-54): the four
+// corner offsets, the in-cell fractions and whether each coordinate is clamped.
+struct Foot {
+  int o00, o10, o01, o11;
+  double fx, fy;
+  bool clx, cly;
+};
+__device__ __forceinline__ Foot footprint(int w, int h, double x, double y) {
+  const Coord cx = cell_coord(x, w), cy = cell_coord(y, h);
+  const int c2 = min(cx.i0 + 1, w - 1), r2 = min(cy.i0 + 1, h - 1);
+  Foot f;
+  f.o00 = cy.i0 * w + cx.i0;
+  f.o10 = cy.i0 * w + c2;
+  f.o01 = r2 * w + cx.i0;
+  f.o11 = r2 * w + c2;
+  f.fx = cx.f;
+  f.fy = cy.f;
+  f.clx = cx.clamped;
+  f.cly = cy.clamped;
+  return f;
+}
+
+// Central-difference pixel gradient (image.cpp:56-77): one-sided at borders.
+__device__ __forceinline__ double2 pixel_grad(const double* __restrict__ I, int w, int h, int x, int y) {
+  const double* R = I + static_cast<size_t>(y) * w;
+  double2 g;
+  g.x = w == 1 ? 0.0 : ((x == 0 || x == w - 1) ? 1.0 : 0.5) * (R[min(x + 1, w - 1)] - R[max(x - 1, 0)]);
+  g.y = h == 1 ? 0.0
+               : ((y == 0 || y == h - 1) ? 1.0 : 0.5) *
+                     (I[static_cast<size_t>(min(y + 1, h - 1)) * w + x] - I[static_cast<size_t>(max(y - 1, 0)) * w + x]);
+  return g;
+}
+
 // warp_grid.cpp:41-54 support for an in-coverage position; returns the cell.
 __device__ __forceinline__ void grid_support(int gw, int gh, int step, double x, double y, int& a0,
                                              int& b0, double& fu, double& fv) {

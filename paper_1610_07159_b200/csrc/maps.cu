@@ -109,17 +109,69 @@ __device__ __forceinline__ void load_tri(const int2* __restrict__ Q, int e, int 
   T.mxy = max(T.Y[0], max(T.Y[1], T.Y[2]));
 }
 
-// int64 edge functions with the top-left tie rule (pin C.2)
-__device__ __forceinline__ bool covers(const Tri& T, long long Px, long long Py) {
-  bool in = true;
+// Coverage of one pixel row, two exact forms of the same integer test (pin C.2):
+// edge i is satisfied at pixel centre Px iff E_i = dx_i (Py - Y_i) - dy_i (Px - X_i)
+// is > 0, or == 0 on a top-left edge (dy > 0, or dy == 0 and dx < 0). Inside a
+// <= 32 px box, coordinates relative to the box origin keep every product and
+// sum below 2^31, so int32 is exact.
+//
+// (a) small boxes: incremental E_i along the row, one test per pixel.
+struct RowEdges {
+  int E[3], step[3];
+  bool tl[3];
+};
+__device__ __forceinline__ void raster_row_tests(const Tri& T, long long yy, long long x0, long long x1, int w,
+                                                 unsigned long long* zb, unsigned long long key) {
+  RowEdges R;
+  const long long Px0 = x0 * 256, Py = yy * 256;
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     const int j = (i + 1) % 3;
-    const long long dx = T.X[j] - T.X[i], dy = T.Y[j] - T.Y[i];
-    const long long E = dx * (Py - T.Y[i]) - dy * (Px - T.X[i]);
-    in = in && (E > 0 || (E == 0 && (dy > 0 || (dy == 0 && dx < 0))));
+    const int dx = static_cast<int>(T.X[j] - T.X[i]), dy = static_cast<int>(T.Y[j] - T.Y[i]);
+    R.E[i] = dx * static_cast<int>(Py - T.Y[i]) - dy * static_cast<int>(Px0 - T.X[i]);
+    R.step[i] = -256 * dy;
+    R.tl[i] = dy > 0 || (dy == 0 && dx < 0);
   }
-  return in;
+  unsigned long long* row = zb + yy * w;
+  for (long long xx = x0; xx <= x1; ++xx) {
+    bool in = true;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) in = in && (R.E[i] > 0 || (R.E[i] == 0 && R.tl[i]));
+    if (in) atomicMin(row + xx, key);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) R.E[i] += R.step[i];
+  }
+}
+
+// (b) large boxes: solve each edge inequality for the covered x-interval, with
+// xx' = xx - x0 and A'_i = dx_i (Py - Y_i) + dy_i (X_i - 256 x0):
+//   dy > 0 (top-left):  E >= 0  <=>  xx' <= floor(A' / (256 dy))
+//   dy < 0:             E >  0  <=>  xx' >= floor(-A' / (256 |dy|)) + 1
+//   dy == 0:            row-constant test.
+__device__ __forceinline__ int floordiv32(int a, int b) {  // b > 0
+  int q = a / b;
+  if ((a % b != 0) && (a < 0)) --q;
+  return q;
+}
+__device__ __forceinline__ void raster_row_span(const Tri& T, long long yy, long long x0, long long x1, int w,
+                                                unsigned long long* zb, unsigned long long key) {
+  int lo = 0, hi = static_cast<int>(x1 - x0);
+  const long long Px0 = x0 * 256, Py = yy * 256;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const int j = (i + 1) % 3;
+    const int dx = static_cast<int>(T.X[j] - T.X[i]), dy = static_cast<int>(T.Y[j] - T.Y[i]);
+    const int A = dx * static_cast<int>(Py - T.Y[i]) + dy * static_cast<int>(T.X[i] - Px0);
+    if (dy > 0) {
+      hi = min(hi, floordiv32(A, 256 * dy));
+    } else if (dy < 0) {
+      lo = max(lo, floordiv32(-A, -256 * dy) + 1);
+    } else if (!(A > 0 || (A == 0 && dx < 0))) {
+      hi = lo - 1;
+    }
+  }
+  unsigned long long* row = zb + yy * w + x0;
+  for (int k = lo; k <= hi; ++k) atomicMin(row + k, key);
 }
 
 constexpr int kSmallBoxPx = 16;  // triangles whose pixel box exceeds this go to the warp queue
@@ -160,12 +212,10 @@ __global__ void k_occ_raster(int w, int h, const int2* __restrict__ q, const flo
   const unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(zf)) << 32) |
                                  static_cast<unsigned int>(tri);
   unsigned long long* zb = zbuf + (static_cast<size_t>(pair) * 4 + e) * N;
-  for (long long yy = y0; yy <= y1; ++yy)
-    for (long long xx = x0; xx <= x1; ++xx)
-      if (covers(T, xx * 256, yy * 256)) atomicMin(zb + yy * w + xx, key);
+  for (long long yy = y0; yy <= y1; ++yy) raster_row_tests(T, yy, x0, x1, w, zb, key);
 }
 
-// Warp per queued large triangle; lanes stride over its pixel box.
+// Warp per queued large triangle; one lane per pixel row of its box.
 __global__ void k_occ_raster_big(int w, int h, const int2* __restrict__ q, const float* __restrict__ Z,
                                  unsigned long long* __restrict__ zbuf, const unsigned long long* __restrict__ queue,
                                  const unsigned int* __restrict__ qcount) {
@@ -187,12 +237,8 @@ __global__ void k_occ_raster_big(int w, int h, const int2* __restrict__ q, const
                                    static_cast<unsigned int>(tri);
     const long long x0 = max(0LL, -((-T.mnx) >> 8)), x1 = min(static_cast<long long>(w - 1), T.mxx >> 8);
     const long long y0 = max(0LL, -((-T.mny) >> 8)), y1 = min(static_cast<long long>(h - 1), T.mxy >> 8);
-    const long long bw = x1 - x0 + 1, nb = bw * (y1 - y0 + 1);
     unsigned long long* zb = zbuf + (static_cast<size_t>(pair) * 4 + e) * N;
-    for (long long k = lane; k < nb; k += 32) {
-      const long long xx = x0 + k % bw, yy = y0 + k / bw;
-      if (covers(T, xx * 256, yy * 256)) atomicMin(zb + yy * w + xx, key);
-    }
+    for (long long yy = y0 + lane; yy <= y1; yy += 32) raster_row_span(T, yy, x0, x1, w, zb, key);
   }
 }
 

@@ -39,9 +39,13 @@ __device__ __forceinline__ double team_sum(double v, double* scratch) {
   return s;
 }
 
-template <int TEAM>
+// NLOC > 0: tiles of <= NLOC nodes, one warp per subdomain, each lane keeps
+// its dense local row (NLOC nodes x 6) in registers. NLOC == 0: general tiles,
+// a team of TEAM threads, 9-slot rows.
+template <int TEAM, int NLOC>
 __global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM) k_schwarz(const SwzArgs a) {
   constexpr int SUBS = TEAM == 32 ? 4 : 1;
+  constexpr int NR = NLOC > 0 ? NLOC : 9;  // row blocks held per lane
   __shared__ double psh[SUBS][TEAM];
   __shared__ double scratch[TEAM / 32 + 1];
   const int team = threadIdx.x / TEAM, u = threadIdx.x % TEAM;
@@ -61,12 +65,24 @@ __global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM) k_schwarz(const SwzAr
   const double* pub = a.pub ? a.pub + static_cast<size_t>(pair) * G * 6 : nullptr;
   double* psub = psh[team];
 
-  double arow[9][6];
-  int lidx[9];
+  double arow[NR][6];
+  int lidx[NR];
   double b = 0.0, x = 0.0;
   if (act) {
     b = __ldg(sys + static_cast<size_t>(n) * kSysStride + kSysRhs + r);
     if (pub) x = __ldg(pub + 6 * static_cast<size_t>(n) + r);
+  }
+  if (NLOC > 0) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {  // dense local row over the tile's nodes
+      const int jx = j % a.nxm, jy = j / a.nxm;
+      const int qa = alo + jx, qb = blo + jy;
+      const bool ok = act && j < a.nxm * a.nym && qa <= ahi && qb <= bhi && abs(qa - na) <= 1 && abs(qb - nb) <= 1;
+      const int s9 = (qb - nb + 1) * 3 + (qa - na + 1);
+      lidx[j] = 6 * j;
+#pragma unroll
+      for (int c = 0; c < 6; ++c) arow[j][c] = ok ? sys_entry(sys, G, n, qb * a.gw + qa, s9, r, c) : 0.0;
+    }
   }
 #pragma unroll
   for (int s9 = 0; s9 < 9; ++s9) {
@@ -75,11 +91,12 @@ __global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM) k_schwarz(const SwzAr
     const bool valid = act && qa >= 0 && qa < a.gw && qb >= 0 && qb < a.gh;
     const bool local = valid && qa >= alo && qa <= ahi && qb >= blo && qb <= bhi;
     const int qn = valid ? qb * a.gw + qa : 0;
-    lidx[s9] = local ? 6 * ((ix + dx) + (iy + dy) * a.nxm) : 0;
+    if (NLOC == 0) lidx[s9] = local ? 6 * ((ix + dx) + (iy + dy) * a.nxm) : 0;
+    if (NLOC > 0 && (local || !valid || !pub)) continue;
 #pragma unroll
     for (int c = 0; c < 6; ++c) {
       const double v = valid ? sys_entry(sys, G, n, qn, s9, r, c) : 0.0;
-      arow[s9][c] = local ? v : 0.0;
+      if (NLOC == 0) arow[s9][c] = local ? v : 0.0;
       if (valid && !local && pub) b -= v * __ldg(pub + 6 * static_cast<size_t>(qn) + c);  // solver.cpp:437-448
     }
   }
@@ -96,9 +113,9 @@ __global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM) k_schwarz(const SwzAr
     if (TEAM == 32) __syncwarp(); else __syncthreads();
     double acc = 0.0;
 #pragma unroll
-    for (int s9 = 0; s9 < 9; ++s9)
+    for (int j = 0; j < NR; ++j)
 #pragma unroll
-      for (int c = 0; c < 6; ++c) acc += arow[s9][c] * psub[lidx[s9] + c];
+      for (int c = 0; c < 6; ++c) acc += arow[j][c] * psub[lidx[j] + c];
     return act ? acc : 0.0;
   };
   auto precond = [&](double rv) {
@@ -270,15 +287,15 @@ __global__ void __launch_bounds__(kPcgThreads) k_pcg_global(const PcgArgs a) {
 
 void launch_schwarz(const SwzArgs& a, int B, cudaStream_t s) {
   const int nsub = a.ntx * a.nty;
-  const int unknowns = 6 * a.nxm * a.nym;
-  if (unknowns <= 32) {
-    k_schwarz<32><<<dim3((nsub + 3) / 4, B), 128, 0, s>>>(a);
-  } else if (unknowns <= 128) {
-    k_schwarz<128><<<dim3(nsub, B), 128, 0, s>>>(a);
-  } else if (unknowns <= 384) {
-    k_schwarz<384><<<dim3(nsub, B), 384, 0, s>>>(a);
+  const int nodes = a.nxm * a.nym;
+  if (nodes <= 4) {
+    k_schwarz<32, 4><<<dim3((nsub + 3) / 4, B), 128, 0, s>>>(a);
+  } else if (6 * nodes <= 128) {
+    k_schwarz<128, 0><<<dim3(nsub, B), 128, 0, s>>>(a);
+  } else if (6 * nodes <= 384) {
+    k_schwarz<384, 0><<<dim3(nsub, B), 384, 0, s>>>(a);
   } else {
-    k_schwarz<1024><<<dim3(nsub, B), 1024, 0, s>>>(a);
+    k_schwarz<1024, 0><<<dim3(nsub, B), 1024, 0, s>>>(a);
   }
 }
 

@@ -23,7 +23,7 @@ void down(T* host, const T* dev, size_t n) {
 }
 
 // Upload one hwf_level into a B=1 LevelDev (solver buffers allocated).
-void load_level(DevMem& m, LevelDev& d, const hwf_level* lv, bool schwarz_tiles, int tile_px) {
+void load_level(DevMem& m, LevelDev& d, const hwf_level* lv, bool schwarz_tiles, int tile_px, cudaStream_t st) {
   if (!lv || lv->width < 1 || lv->height < 1) throw InvalidArg("bad level");
   if (lv->grid_step < 1 || lv->grid_step > 32) throw InvalidArg("grid_step must be in [1, 32] on the device");
   d.dims(lv->width, lv->height, lv->grid_step, schwarz_tiles ? tile_px : 0);
@@ -33,6 +33,8 @@ void load_level(DevMem& m, LevelDev& d, const hwf_level* lv, bool schwarz_tiles,
     if (!lv->images[e]) throw InvalidArg("null image");
     CK(cudaMemcpy(d.img + e * d.N, lv->images[e], d.N * sizeof(double), cudaMemcpyHostToDevice));
   }
+  d.grad = m.alloc<double2>(4 * d.N);
+  launch_grad(d.img, d.w, d.h, 4, d.grad, st);
   bool any = false;
   for (int e = 0; e < 4; ++e) any = any || lv->illum[e];
   if (any) {
@@ -71,7 +73,7 @@ PixArgs pix_args(const LevelDev& d, const hwf_energy_params* P, uint32_t active,
   PixArgs pa{};
   pa.w = d.w; pa.h = d.h; pa.gw = d.gw; pa.gh = d.gh; pa.step = d.step; pa.ncx = d.ncx; pa.ncy = d.ncy;
   pa.tcx = d.tcx; pa.tcy = d.tcy; pa.rp = d.rp;
-  pa.img = d.img; pa.illum = d.illum; pa.vis4 = d.vis; pa.W = d.W; pa.total = d.total; pa.half = d.half;
+  pa.img = d.img; pa.grad = d.grad; pa.illum = d.illum; pa.vis4 = d.vis; pa.W = d.W; pa.total = d.total; pa.half = d.half;
   pa.cells = d.cells; pa.ep_pair = E.pair_stride(); pa.flags = flags; pa.P = to_params(*P);
   pa.active = active; pa.ep_new = E.slot(0);
   return pa;
@@ -196,7 +198,7 @@ int hwf_eval_energy(hwf_ctx* ctx, const hwf_level* lv, const hwf_energy_params* 
     if (residuals) throw InvalidArg("residual vector output is not provided by the device library");
     DevMem m;
     LevelDev d;
-    load_level(m, d, lv, false, 0);
+    load_level(m, d, lv, false, 0, ctx->stream);
     const double* dF = lv->fundamental ? up(m, lv->fundamental, 9) : nullptr;
     Energies E;
     make_energies(m, E, d, 1);
@@ -228,7 +230,7 @@ int hwf_refresh_weights(hwf_ctx* ctx, const hwf_level* lv, const hwf_energy_para
   return guard(ctx, [&] {
     DevMem m;
     LevelDev d;
-    load_level(m, d, lv, false, 0);
+    load_level(m, d, lv, false, 0, ctx->stream);
     const double* dF = lv->fundamental ? up(m, lv->fundamental, 9) : nullptr;
     Energies E;
     make_energies(m, E, d, 1);
@@ -252,7 +254,7 @@ int hwf_linearize(hwf_ctx* ctx, const hwf_level* lv, const hwf_energy_params* P,
     if (P->w_epi > 0.0 && !lv->fundamental) throw InvalidArg("epipolar term enabled without a fundamental matrix");
     DevMem m;
     LevelDev d;
-    load_level(m, d, lv, false, 0);
+    load_level(m, d, lv, false, 0, ctx->stream);
     const double* dF = lv->fundamental ? up(m, lv->fundamental, 9) : nullptr;
     Energies E;
     make_energies(m, E, d, 1);
@@ -345,7 +347,7 @@ int hwf_gn_level(hwf_ctx* ctx, const hwf_level* lv, const double* base, double* 
     l2.outlier = outlier;
     l2.node_w = node_w;
     l2.delta = delta;
-    load_level(m, d, &l2, S->subdomain_px > 0, S->subdomain_px);
+    load_level(m, d, &l2, S->subdomain_px > 0, S->subdomain_px, ctx->stream);
     std::vector<double> tot(6 * d.G);
     for (size_t i = 0; i < tot.size(); ++i) tot[i] = base[i] + delta[i];  // base.plus(delta)
     CK(cudaMemcpy(d.total, tot.data(), tot.size() * sizeof(double), cudaMemcpyHostToDevice));
