@@ -17,7 +17,9 @@
 //       UL triangle is not degenerate and the front-most triangle at
 //       round(P_e(x)) is one of the six triangles incident to x, or is not
 //       nearer than z(x) by more than 1e-4. Degenerate: area <= 0, non-finite
-//       flow, or a bounding box wider/taller than 32 px.
+//       flow, or a bounding box wider/taller than 8 px (a rubber-sheet triangle
+//       spanning a flow discontinuity of > 8 px per lattice cell is not a surface:
+//       it would over-occlude the band beside a foreground edge).
 //   C.3 vis4 bit e = that per-view visibility; V_k = AND of endpoints
 //       (energy.hpp:65-68). Mask prolongation: bilinear of the 0/1 plane at
 //       x/2 (image.cpp sample semantics), visible iff >= 0.5.
@@ -42,7 +44,7 @@ struct hwf_ctx {
 namespace orc {
 namespace {
 
-constexpr int kZbufSpanPx = 32;
+constexpr int kZbufSpanPx = 8;
 constexpr double kDepthTol = 1e-4;
 constexpr double kIllumSigma = 3.2;
 

@@ -68,7 +68,7 @@ struct LevelDev {
   int w = 0, h = 0, gw = 0, gh = 0, step = 0, ncx = 0, ncy = 0, tcx = 0, tcy = 0, rp = 0;
   int ntx = 0, nty = 0, nxm = 0, nym = 0, tile = 0;
   size_t N = 0, G = 0, C = 0;
-  double2* grad = nullptr;
+  double4* pk = nullptr;
   double *img = nullptr, *illum = nullptr, *base = nullptr, *delta = nullptr, *total = nullptr;
   double *nodew = nullptr, *half = nullptr, *cells = nullptr, *sys = nullptr, *xa = nullptr, *xb = nullptr,
          *hm = nullptr;
@@ -178,7 +178,7 @@ inline void record_gn_level(LevelDev& d, int B, const hwf_energy_params& P, cons
   PixArgs pa{};
   pa.w = d.w; pa.h = d.h; pa.gw = d.gw; pa.gh = d.gh; pa.step = d.step; pa.ncx = d.ncx; pa.ncy = d.ncy;
   pa.tcx = d.tcx; pa.tcy = d.tcy; pa.rp = d.rp;
-  pa.img = d.img; pa.grad = d.grad; pa.illum = d.illum; pa.vis4 = d.vis; pa.W = d.W; pa.total = d.total; pa.half = d.half;
+  pa.pk = d.pk; pa.illum = d.illum; pa.vis4 = d.vis; pa.W = d.W; pa.total = d.total; pa.half = d.half;
   pa.cells = d.cells; pa.ep_pair = E.pair_stride(); pa.flags = flags; pa.P = to_params(P);
   pa.active = S.active_fields; pa.refresh = 1;
   NodeArgs na{};
@@ -293,7 +293,7 @@ struct Plan {
     for (int l = 0; l < L; ++l) {
       LevelDev& d = lv[l];
       d.img = mem.alloc<double>(B * 4 * d.N);
-      d.grad = mem.alloc<double2>(B * 4 * d.N);
+      d.pk = mem.alloc<double4>(B * 4 * d.N);
       d.alloc_solver(mem, B, S.subdomain_px > 0);
       d.occ = mem.alloc<uint8_t>(B * d.N);
       if (l < L - 1) d.illum = mem.alloc<double>(B * 4 * d.N);
@@ -350,7 +350,7 @@ struct Plan {
       LC.count++;
     }
     for (int l = 0; l < L; ++l) {
-      launch_grad(lv[l].img, lv[l].w, lv[l].h, 4 * B, lv[l].grad, st);
+      launch_pack(lv[l].img, lv[l].w, lv[l].h, 4 * B, lv[l].pk, st);
       LC.count++;
     }
     for (int l = L - 1; l >= 0; --l) {

@@ -12,7 +12,7 @@ namespace hwf {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kZbufSpanPx = 32;   // oracle/hierarchy.cpp pin C.2
+constexpr int kZbufSpanPx = 8;    // oracle/hierarchy.cpp pin C.2
 constexpr double kDepthTol = 1e-4;
 
 // ---- pyramid (image.cpp:100-122, 177-185) -----------------
@@ -112,7 +112,7 @@ __device__ __forceinline__ void load_tri(const int2* __restrict__ Q, int e, int 
 // Coverage of one pixel row, two exact forms of the same integer test (pin C.2):
 // edge i is satisfied at pixel centre Px iff E_i = dx_i (Py - Y_i) - dy_i (Px - X_i)
 // is > 0, or == 0 on a top-left edge (dy > 0, or dy == 0 and dx < 0). Inside a
-// <= 32 px box, coordinates relative to the box origin keep every product and
+// <= 8 px box, coordinates relative to the box origin keep every product and
 // sum below 2^31, so int32 is exact.
 //
 // (a) small boxes: incremental E_i along the row, one test per pixel.
