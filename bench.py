@@ -157,12 +157,19 @@ def dist_init():
     return ws, rank, local
 
 
+def shard(rank: int, ws: int, per_gpu: int) -> range:
+    """Frame mode: rank r owns global pairs [r*B, (r+1)*B); no collective."""
+    return range(rank * per_gpu, (rank + 1) * per_gpu)
+
+
 def allreduce_max(x: float, ws: int) -> float:
+    """Max over ranks of a device-timed duration (the only cross-rank traffic)."""
     if ws == 1:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -206,7 +213,8 @@ def run_ours(args, ws, rank, local):
     G = gw * gh
 
     # inputs: B distinct pairs for this rank (seeds 1610 + global pair index), pinned host copy
-    frames_np = make_frames(B, rank * B)
+    pairs = shard(rank, ws, B)
+    frames_np = make_frames(B, pairs.start)
     host_in = torch.from_numpy(frames_np).pin_memory()
     host_grid = torch.empty((B, G, 6), dtype=torch.float64).pin_memory()
     host_vis = torch.empty((B, H_, W_), dtype=torch.uint8).pin_memory()

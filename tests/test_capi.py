@@ -4,6 +4,7 @@ the product fails loudly (no CPU fallback)."""
 from __future__ import annotations
 
 import ctypes as C
+from pathlib import Path
 import re
 import subprocess
 
@@ -97,3 +98,16 @@ def test_synthetic_pull_back_is_exact():
     b = synthetic.render_pair(64, 48, s=s, m=m, seed=5, noise=0.0, dtype=np.float64)
     assert np.allclose(b[1][:, 2:], b[0][:, :-2])  # right = left shifted by disparity 2 s_x
     assert a.shape == (4, 48, 64) and T(*x).shape == (2,)
+
+
+def test_reference_side_bridge_compiles():
+    """include/hwflow_bridge.hpp (the adapter a reference maintainer adds) compiles
+    against the reference's own headers (with the Eigen shim)."""
+    ref_inc = Path("/root/reference/proj/include")
+    if not ref_inc.exists():
+        pytest.skip("reference headers not present")
+    src = "#include \"hwflow_bridge.hpp\"\nint main() { return 0; }\n"
+    r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-x", "c++", "-", f"-I{ROOT / 'include'}",
+                        f"-I{ROOT / 'oracle' / 'eigen_shim'}", f"-I{ref_inc}"], input=src, capture_output=True,
+                       text=True)
+    assert r.returncode == 0, r.stderr[-2000:]
