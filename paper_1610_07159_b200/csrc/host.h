@@ -167,7 +167,8 @@ struct Launches {
 // Algorithmic bytes of one k_pixel<LIN> launch: every
 // input read once, every output written once.
 inline double pixel_bytes(const LevelDev& d, int B, bool illum) {
-  const double perpix = 4 * 8.0 + (illum ? 4 * 8.0 : 0.0) + 1 + 1 + 1 + 8;
+  // packed {v, gx, gy, pad} samples of 4 images, illumination, vis4 + W in/out, halfway out
+  const double perpix = 4 * 32.0 + (illum ? 4 * 8.0 : 0.0) + 1 + 1 + 1 + 8;
   return B * (d.N * perpix + d.G * 48.0 + d.C * kCellStride * 8.0);
 }
 
