@@ -79,7 +79,7 @@ __global__ void k_occ_project(int w, int h, int gw, int gh, int step, const doub
     int2 v;
     v.x = ok ? static_cast<int>(__double2ll_rn(fx)) : 0;
     v.y = ok ? static_cast<int>(__double2ll_rn(fy)) : 0;
-    q[(pair * N + pix) * 4 + e] = v;
+    q[(pair * 4 + e) * N + pix] = v;  // view-major: a triangle's vertices are contiguous
   }
   bad[pair * N + pix] = ok ? 0 : 1;
 }
@@ -98,9 +98,7 @@ __device__ __forceinline__ void tri_vertices(int w, long long tri, int& v0, int&
   v2 = (cy + 1) * w + cx;
 }
 
-__device__ __forceinline__ void load_tri(const int2* __restrict__ Q, int e, int v0, int v1, int v2, Tri& T) {
-  const int2 p0 = Q[4 * static_cast<size_t>(v0) + e], p1 = Q[4 * static_cast<size_t>(v1) + e],
-             p2 = Q[4 * static_cast<size_t>(v2) + e];
+__device__ __forceinline__ void make_tri(int2 p0, int2 p1, int2 p2, Tri& T) {
   T.X[0] = p0.x; T.X[1] = p1.x; T.X[2] = p2.x;
   T.Y[0] = p0.y; T.Y[1] = p1.y; T.Y[2] = p2.y;
   T.mnx = min(T.X[0], min(T.X[1], T.X[2]));
@@ -176,43 +174,53 @@ __device__ __forceinline__ void raster_row_span(const Tri& T, long long yy, long
 
 constexpr int kSmallBoxPx = 16;  // triangles whose pixel box exceeds this go to the warp queue
 
-// One thread per (triangle, view, pair). Degeneracy test, flat depth key,
-// small boxes rasterised in-thread; large boxes queued for k_occ_raster_big.
+// One triangle: degeneracy test, flat depth key, in-thread raster of small
+// boxes, queue for large boxes. Returns whether the triangle is degenerate.
+__device__ __forceinline__ bool raster_tri(int w, int h, const Tri& T, bool any_bad, float zf, unsigned int tri,
+                                           unsigned long long* zb, unsigned long long* queue,
+                                           unsigned int* qcount, unsigned long long qtag) {
+  const long long area = (T.X[1] - T.X[0]) * (T.Y[2] - T.Y[0]) - (T.Y[1] - T.Y[0]) * (T.X[2] - T.X[0]);
+  const bool deg = any_bad || area <= 0 || (T.mxx - T.mnx) > kZbufSpanPx * 256 || (T.mxy - T.mny) > kZbufSpanPx * 256;
+  if (deg) return true;
+  const long long x0 = max(0LL, -((-T.mnx) >> 8)), x1 = min(static_cast<long long>(w - 1), T.mxx >> 8);
+  const long long y0 = max(0LL, -((-T.mny) >> 8)), y1 = min(static_cast<long long>(h - 1), T.mxy >> 8);
+  if (x1 < x0 || y1 < y0) return false;
+  if ((x1 - x0 + 1) * (y1 - y0 + 1) > kSmallBoxPx) {
+    queue[atomicAdd(qcount, 1u)] = qtag | tri;
+    return false;
+  }
+  const unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(zf)) << 32) | tri;
+  for (long long yy = y0; yy <= y1; ++yy) raster_row_tests(T, yy, x0, x1, w, zb, key);
+  return false;
+}
+
+// One thread per (lattice cell, view, pair): both triangles of the cell (pin C.2),
+// UL {(x,y),(x+1,y),(x,y+1)} then LR {(x+1,y),(x+1,y+1),(x,y+1)}, sharing 4 vertices.
 // atomicMin on (depth bits, triangle id) makes the z-buffer order-independent.
 __global__ void k_occ_raster(int w, int h, const int2* __restrict__ q, const float* __restrict__ Z,
                              const uint8_t* __restrict__ bad, unsigned long long* __restrict__ zbuf,
                              uint8_t* __restrict__ degen, unsigned long long* __restrict__ queue,
                              unsigned int* __restrict__ qcount) {
-  const long long ntri = 2LL * (w - 1) * (h - 1);
-  const long long tri = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  const int e = blockIdx.y, pair = blockIdx.z;
-  if (tri >= ntri) return;
+  const int cw = w - 1;
+  const int cx = blockIdx.x * blockDim.x + threadIdx.x, cy = blockIdx.y / 4, e = blockIdx.y % 4, pair = blockIdx.z;
+  if (cx >= cw) return;
   const size_t N = static_cast<size_t>(w) * h;
-  int v0, v1, v2;
-  tri_vertices(w, tri, v0, v1, v2);
+  const int i00 = cy * w + cx, i10 = i00 + 1, i01 = i00 + w, i11 = i01 + 1;
+  const int2* Q = q + (static_cast<size_t>(pair) * 4 + e) * N;
   const uint8_t* B = bad + pair * N;
-  Tri T;
-  load_tri(q + pair * N * 4, e, v0, v1, v2, T);
-  const long long area = (T.X[1] - T.X[0]) * (T.Y[2] - T.Y[0]) - (T.Y[1] - T.Y[0]) * (T.X[2] - T.X[0]);
-  const bool deg = B[v0] || B[v1] || B[v2] || area <= 0 || (T.mxx - T.mnx) > kZbufSpanPx * 256 ||
-                   (T.mxy - T.mny) > kZbufSpanPx * 256;
-  if ((tri & 1) == 0) degen[(static_cast<size_t>(pair) * 4 + e) * N + v0] = deg ? 1 : 0;
-  if (deg) return;
-  const long long x0 = max(0LL, -((-T.mnx) >> 8)), x1 = min(static_cast<long long>(w - 1), T.mxx >> 8);
-  const long long y0 = max(0LL, -((-T.mny) >> 8)), y1 = min(static_cast<long long>(h - 1), T.mxy >> 8);
-  if (x1 < x0 || y1 < y0) return;
-  if ((x1 - x0 + 1) * (y1 - y0 + 1) > kSmallBoxPx) {
-    const unsigned int slot = atomicAdd(qcount, 1u);
-    queue[slot] = (static_cast<unsigned long long>(pair) << 34) | (static_cast<unsigned long long>(e) << 32) |
-                  static_cast<unsigned long long>(tri);
-    return;
-  }
   const float* ZZ = Z + pair * N;
-  const float zf = fminf(ZZ[v0], fminf(ZZ[v1], ZZ[v2]));
-  const unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(zf)) << 32) |
-                                 static_cast<unsigned int>(tri);
+  const int2 p00 = Q[i00], p10 = Q[i10], p01 = Q[i01], p11 = Q[i11];
+  const bool b00 = B[i00], b10 = B[i10], b01 = B[i01], b11 = B[i11];
+  const float z00 = ZZ[i00], z10 = ZZ[i10], z01 = ZZ[i01], z11 = ZZ[i11];
   unsigned long long* zb = zbuf + (static_cast<size_t>(pair) * 4 + e) * N;
-  for (long long yy = y0; yy <= y1; ++yy) raster_row_tests(T, yy, x0, x1, w, zb, key);
+  const unsigned long long qtag = (static_cast<unsigned long long>(pair) << 34) | (static_cast<unsigned long long>(e) << 32);
+  const unsigned int tri0 = static_cast<unsigned int>(2 * (cy * cw + cx));
+  Tri T;
+  make_tri(p00, p10, p01, T);
+  const bool d0 = raster_tri(w, h, T, b00 || b10 || b01, fminf(z00, fminf(z10, z01)), tri0, zb, queue, qcount, qtag);
+  degen[(static_cast<size_t>(pair) * 4 + e) * N + i00] = d0 ? 1 : 0;
+  make_tri(p10, p11, p01, T);
+  raster_tri(w, h, T, b10 || b11 || b01, fminf(z10, fminf(z11, z01)), tri0 + 1, zb, queue, qcount, qtag);
 }
 
 // Warp per queued large triangle; one lane per pixel row of its box.
@@ -229,8 +237,9 @@ __global__ void k_occ_raster_big(int w, int h, const int2* __restrict__ q, const
     const long long tri = static_cast<long long>(item & 0xffffffffULL);
     int v0, v1, v2;
     tri_vertices(w, tri, v0, v1, v2);
+    const int2* Q = q + (static_cast<size_t>(pair) * 4 + e) * N;
     Tri T;
-    load_tri(q + pair * N * 4, e, v0, v1, v2, T);
+    make_tri(Q[v0], Q[v1], Q[v2], T);
     const float* ZZ = Z + pair * N;
     const float zf = fminf(ZZ[v0], fminf(ZZ[v1], ZZ[v2]));
     const unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(zf)) << 32) |
@@ -262,7 +271,7 @@ __global__ void k_occ_resolve(int w, int h, const int2* __restrict__ q, const fl
     bool v = !b;
     if (v && px < w - 1 && py < h - 1 && degen[(static_cast<size_t>(pair) * 4 + e) * N + pix]) v = false;
     if (v) {
-      const int2 qq = q[(pair * N + pix) * 4 + e];
+      const int2 qq = q[(static_cast<size_t>(pair) * 4 + e) * N + pix];
       const long long rx = (static_cast<long long>(qq.x) + 128) >> 8, ry = (static_cast<long long>(qq.y) + 128) >> 8;
       if (rx >= 0 && rx < w && ry >= 0 && ry < h) {
         const unsigned long long key = zbuf[(static_cast<size_t>(pair) * 4 + e) * N + ry * w + rx];
@@ -464,8 +473,7 @@ void launch_occlusion(int w, int h, int gw, int gh, int step, const double* tota
   if (w >= 2 && h >= 2) {
     cudaMemsetAsync(zbuf, 0xFF, N * 4 * B * sizeof(unsigned long long), s);
     cudaMemsetAsync(qcount, 0, sizeof(unsigned int), s);
-    const long long ntri = 2LL * (w - 1) * (h - 1);
-    k_occ_raster<<<dim3(static_cast<unsigned>((ntri + kThreads - 1) / kThreads), 4, B), kThreads, 0, s>>>(
+    k_occ_raster<<<dim3((w - 1 + kThreads - 1) / kThreads, 4 * (h - 1), B), kThreads, 0, s>>>(
         w, h, q, Z, bad, zbuf, degen, queue, qcount);
     k_occ_raster_big<<<148 * 8, kThreads, 0, s>>>(w, h, q, Z, zbuf, queue, qcount);
   }

@@ -68,8 +68,13 @@ __global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM) k_schwarz(const SwzAr
   double arow[NR][6];
   int lidx[NR];
   double b = 0.0, x = 0.0;
+  // packed offsets of row r in a symmetric 6x6 block: sym6(r, c) for c = 0..5
+  int ro[6];
+#pragma unroll
+  for (int c = 0; c < 6; ++c) ro[c] = sym6(r, c);
+  const double* sysn = sys + static_cast<size_t>(n) * kSysStride;
   if (act) {
-    b = __ldg(sys + static_cast<size_t>(n) * kSysStride + kSysRhs + r);
+    b = __ldg(sysn + kSysRhs + r);
     if (pub) x = __ldg(pub + 6 * static_cast<size_t>(n) + r);
   }
   if (NLOC > 0) {
@@ -79,25 +84,48 @@ __global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM) k_schwarz(const SwzAr
       const int qa = alo + jx, qb = blo + jy;
       const bool ok = act && j < a.nxm * a.nym && qa <= ahi && qb <= bhi && abs(qa - na) <= 1 && abs(qb - nb) <= 1;
       const int s9 = (qb - nb + 1) * 3 + (qa - na + 1);
+      const double* blk = s9 >= 4 ? sysn + (s9 - 4) * 21 : sys + static_cast<size_t>(qb * a.gw + qa) * kSysStride + (4 - s9) * 21;
       lidx[j] = 6 * j;
 #pragma unroll
-      for (int c = 0; c < 6; ++c) arow[j][c] = ok ? sys_entry(sys, G, n, qb * a.gw + qa, s9, r, c) : 0.0;
+      for (int c = 0; c < 6; ++c) arow[j][c] = ok ? __ldg(blk + ro[c]) : 0.0;
     }
   }
+  if (NLOC > 0 && pub) {
+    // coupling to the frozen neighbours (solver.cpp:437-448), two alternating chains
+    double b0 = 0.0, b1 = 0.0;
 #pragma unroll
-  for (int s9 = 0; s9 < 9; ++s9) {
-    const int dx = s9 % 3 - 1, dy = s9 / 3 - 1;
-    const int qa = na + dx, qb = nb + dy;
-    const bool valid = act && qa >= 0 && qa < a.gw && qb >= 0 && qb < a.gh;
-    const bool local = valid && qa >= alo && qa <= ahi && qb >= blo && qb <= bhi;
-    const int qn = valid ? qb * a.gw + qa : 0;
-    if (NLOC == 0) lidx[s9] = local ? 6 * ((ix + dx) + (iy + dy) * a.nxm) : 0;
-    if (NLOC > 0 && (local || !valid || !pub)) continue;
+    for (int s9 = 0; s9 < 9; ++s9) {
+      if (s9 == 4) continue;
+      const int qa = na + s9 % 3 - 1, qb = nb + s9 / 3 - 1;
+      const bool valid = act && qa >= 0 && qa < a.gw && qb >= 0 && qb < a.gh;
+      const bool local = qa >= alo && qa <= ahi && qb >= blo && qb <= bhi;
+      if (!valid || local) continue;
+      const int qn = qb * a.gw + qa;
+      const double* blk = s9 >= 4 ? sysn + (s9 - 4) * 21 : sys + static_cast<size_t>(qn) * kSysStride + (4 - s9) * 21;
+      const double* pv = pub + 6 * static_cast<size_t>(qn);
 #pragma unroll
-    for (int c = 0; c < 6; ++c) {
-      const double v = valid ? sys_entry(sys, G, n, qn, s9, r, c) : 0.0;
-      if (NLOC == 0) arow[s9][c] = local ? v : 0.0;
-      if (valid && !local && pub) b -= v * __ldg(pub + 6 * static_cast<size_t>(qn) + c);  // solver.cpp:437-448
+      for (int c = 0; c < 6; c += 2) {
+        b0 += __ldg(blk + ro[c]) * __ldg(pv + c);
+        b1 += __ldg(blk + ro[c + 1]) * __ldg(pv + c + 1);
+      }
+    }
+    b -= b0 + b1;
+  }
+  if (NLOC == 0) {
+#pragma unroll
+    for (int s9 = 0; s9 < 9; ++s9) {
+      const int dx = s9 % 3 - 1, dy = s9 / 3 - 1;
+      const int qa = na + dx, qb = nb + dy;
+      const bool valid = act && qa >= 0 && qa < a.gw && qb >= 0 && qb < a.gh;
+      const bool local = valid && qa >= alo && qa <= ahi && qb >= blo && qb <= bhi;
+      const int qn = valid ? qb * a.gw + qa : 0;
+      lidx[s9] = local ? 6 * ((ix + dx) + (iy + dy) * a.nxm) : 0;
+#pragma unroll
+      for (int c = 0; c < 6; ++c) {
+        const double v = valid ? sys_entry(sys, G, n, qn, s9, r, c) : 0.0;
+        arow[s9][c] = local ? v : 0.0;
+        if (valid && !local && pub) b -= v * __ldg(pub + 6 * static_cast<size_t>(qn) + c);  // solver.cpp:437-448
+      }
     }
   }
   // preconditioner of this unknown's field (solver.cpp:468-474)
