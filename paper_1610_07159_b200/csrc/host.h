@@ -68,7 +68,8 @@ struct LevelDev {
   int w = 0, h = 0, gw = 0, gh = 0, step = 0, ncx = 0, ncy = 0, tcx = 0, tcy = 0, rp = 0;
   int ntx = 0, nty = 0, nxm = 0, nym = 0, tile = 0;
   size_t N = 0, G = 0, C = 0;
-  double4* pk = nullptr;
+  double2* pk = nullptr;
+  double* gy = nullptr;
   double *img = nullptr, *illum = nullptr, *base = nullptr, *delta = nullptr, *total = nullptr;
   double *nodew = nullptr, *half = nullptr, *cells = nullptr, *sys = nullptr, *xa = nullptr, *xb = nullptr,
          *hm = nullptr;
@@ -167,8 +168,8 @@ struct Launches {
 // Algorithmic bytes of one k_pixel<LIN> launch: every
 // input read once, every output written once.
 inline double pixel_bytes(const LevelDev& d, int B, bool illum) {
-  // packed {v, gx, gy, pad} samples of 4 images, illumination, vis4 + W in/out, halfway out
-  const double perpix = 4 * 32.0 + (illum ? 4 * 8.0 : 0.0) + 1 + 1 + 1 + 8;
+  // {v, gx} + gy samples of 4 images, illumination, vis4 + W in/out, halfway out
+  const double perpix = 4 * 24.0 + (illum ? 4 * 8.0 : 0.0) + 1 + 1 + 1 + 8;
   return B * (d.N * perpix + d.G * 48.0 + d.C * kCellStride * 8.0);
 }
 
@@ -179,7 +180,7 @@ inline void record_gn_level(LevelDev& d, int B, const hwf_energy_params& P, cons
   PixArgs pa{};
   pa.w = d.w; pa.h = d.h; pa.gw = d.gw; pa.gh = d.gh; pa.step = d.step; pa.ncx = d.ncx; pa.ncy = d.ncy;
   pa.tcx = d.tcx; pa.tcy = d.tcy; pa.rp = d.rp;
-  pa.pk = d.pk; pa.illum = d.illum; pa.vis4 = d.vis; pa.W = d.W; pa.total = d.total; pa.half = d.half;
+  pa.pk = d.pk; pa.gy = d.gy; pa.illum = d.illum; pa.vis4 = d.vis; pa.W = d.W; pa.total = d.total; pa.half = d.half;
   pa.cells = d.cells; pa.ep_pair = E.pair_stride(); pa.flags = flags; pa.P = to_params(P);
   pa.active = S.active_fields; pa.refresh = 1;
   NodeArgs na{};
@@ -294,7 +295,8 @@ struct Plan {
     for (int l = 0; l < L; ++l) {
       LevelDev& d = lv[l];
       d.img = mem.alloc<double>(B * 4 * d.N);
-      d.pk = mem.alloc<double4>(B * 4 * d.N);
+      d.pk = mem.alloc<double2>(B * 4 * d.N);
+      d.gy = mem.alloc<double>(B * 4 * d.N);
       d.alloc_solver(mem, B, S.subdomain_px > 0);
       d.occ = mem.alloc<uint8_t>(B * d.N);
       if (l < L - 1) d.illum = mem.alloc<double>(B * 4 * d.N);
@@ -351,7 +353,7 @@ struct Plan {
       LC.count++;
     }
     for (int l = 0; l < L; ++l) {
-      launch_pack(lv[l].img, lv[l].w, lv[l].h, 4 * B, lv[l].pk, st);
+      launch_pack(lv[l].img, lv[l].w, lv[l].h, 4 * B, lv[l].pk, lv[l].gy, st);
       LC.count++;
     }
     for (int l = L - 1; l >= 0; --l) {

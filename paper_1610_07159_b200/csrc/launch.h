@@ -19,7 +19,8 @@ enum : int {
 
 struct PixArgs {
   int w, h, gw, gh, step, ncx, ncy, tcx, tcy, rp;
-  const double4* pk;    // [B][4][N] packed {value, grad x, grad y, 0} (k_pack)
+  const double2* pk;    // [B][4][N] {value, grad x} (k_pack)
+  const double* gy;     // [B][4][N] grad y (k_pack)
   const double* illum;  // [B][4][N] or null
   const uint8_t* vis4;  // [B][N]
   uint8_t* W;           // [B][N] in: current bits; out: refreshed bits (refresh)
@@ -92,7 +93,7 @@ int pixel_tile_cells_y(int step);
 int pixel_smem_pitch(int step);
 size_t pixel_smem_bytes(int step);
 void launch_pixel(bool lin, const PixArgs& a, int B, cudaStream_t s);
-void launch_pack(const double* img, int w, int h, int planes, double4* pk, cudaStream_t s);
+void launch_pack(const double* img, int w, int h, int planes, double2* pk, double* gy, cudaStream_t s);
 int node_ctas(int G);
 void launch_node(bool lin, const NodeArgs& a, int B, cudaStream_t s);
 
