@@ -231,11 +231,15 @@ __device__ __forceinline__ void interp_fast(const double* __restrict__ T, int gw
   double fu, fv;
   grid_support(gw, gh, step, x, y, a0, b0, fu, fv);
   const double w0 = (1 - fu) * (1 - fv), w1 = fu * (1 - fv), w2 = (1 - fu) * fv, w3 = fu * fv;
-  const double* n0 = T + 6 * static_cast<size_t>(b0 * gw + a0);
-  const double* n2 = T + 6 * static_cast<size_t>((b0 + 1) * gw + a0);
+  // node records are 48 B (16 B aligned): three 16-byte loads per node
+  const double2* n0 = reinterpret_cast<const double2*>(T + 6 * static_cast<size_t>(b0 * gw + a0));
+  const double2* n2 = reinterpret_cast<const double2*>(T + 6 * static_cast<size_t>((b0 + 1) * gw + a0));
 #pragma unroll
-  for (int c = 0; c < 6; ++c)
-    out[c] = w0 * __ldg(n0 + c) + w1 * __ldg(n0 + 6 + c) + w2 * __ldg(n2 + c) + w3 * __ldg(n2 + 6 + c);
+  for (int c = 0; c < 3; ++c) {
+    const double2 p0 = __ldg(n0 + c), p1 = __ldg(n0 + 3 + c), p2 = __ldg(n2 + c), p3 = __ldg(n2 + 3 + c);
+    out[2 * c] = w0 * p0.x + w1 * p1.x + w2 * p2.x + w3 * p3.x;
+    out[2 * c + 1] = w0 * p0.y + w1 * p1.y + w2 * p2.y + w3 * p3.y;
+  }
 }
 
 // warp_grid.hpp:74-77 (sigma_0 = -1, sigma_1 = +1); exact adds in reference order.
