@@ -48,6 +48,41 @@ def workload_desc(mode: str) -> str:
     return f"cfg2: 640x480 pairs, 4-level pyramid, 8 px warp grid, GN 2,2,5,5, {solve}, live preset"
 
 
+def extra_configs(dev, lib, h, C, capi, reps: int = 5) -> dict:
+    """The other BASELINE.json shapes on this GPU, device-resident replays (not the headline):
+    cfg3 1920x1080 occluder + illumination change, 5 levels, 8 px grid, batch 4;
+    cfg5 3840x2160 single frame pair, 5 levels, 4 px grid (north_star: >= 30 Hz)."""
+    from paper_1610_07159_b200 import synthetic
+    from paper_1610_07159_b200.hwflow import EnergyParams, SolveSchedule
+    out = {}
+    cases = [("cfg3_1920x1080_batch4", lambda: np.stack([synthetic.valgaerts_pair(i)[0] for i in range(4)]),
+              SolveSchedule(levels=5, grid_step=8, pcg_iters=5, patch_iters=5)),
+             ("cfg5_3840x2160_single_frame", lambda: synthetic.uhd_pair(0)[0][None],
+              SolveSchedule(levels=5, grid_step=4, pcg_iters=5, patch_iters=5))]
+    for name, frames_fn, sched in cases:
+        frames = frames_fn()
+        n = frames.shape[0]
+        try:
+            dev.solve_batch(frames, EnergyParams(), sched, outputs=("grid_total",))
+            status = "ok"
+        except capi.SolverDivergence:
+            status = "diverged-flag"
+        import torch
+        stream = torch.cuda.ExternalStream(lib.hwf_stream(h))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        lib.hwf_run_device(h)
+        e0.record(stream)
+        for _ in range(reps):
+            lib.hwf_run_device(h)
+        e1.record(stream)
+        e1.synchronize()
+        lib.hwf_sync(h, None)
+        ms = e0.elapsed_time(e1) / reps
+        out[name] = {"pairs": n, "ms_per_step": ms, "pairs_per_s": 1000.0 * n / ms,
+                     "solver_status": status, "launches_per_step": lib.hwf_launch_count(h)}
+    return out
+
+
 def make_frames(n: int, first: int) -> np.ndarray:
     from paper_1610_07159_b200 import synthetic
     return np.stack([synthetic.webcam_pair(first + i, W_, H_)[0] for i in range(n)])
@@ -293,6 +328,7 @@ def run_ours(args, ws, rank, local):
     e2e_value = ws * B * args.steps / e2e_s
 
     gn_total = sum(S.gn_for_level(l) for l in range(4))
+    extra = extra_configs(dev, lib, h, C, capi) if (rank == 0 and ws == 1 and not args.no_extra) else None
     if rank == 0:
         cb = cpu_baseline(max(1, min(3, args.steps)), 1, args.mode) if ws == 1 and not args.no_cpu else None
         line = {
@@ -317,6 +353,8 @@ def run_ours(args, ws, rank, local):
         }
         if cb:
             line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        if extra:
+            line["other_configs"] = extra
         print(json.dumps(line), flush=True)
 
 
@@ -329,6 +367,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--mode", choices=["schwarz", "global"], default="schwarz")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-extra", action="store_true", help="skip the cfg3/cfg5 side measurements")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     ws, rank, local = (1, 0, 0)

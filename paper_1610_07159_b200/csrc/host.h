@@ -71,7 +71,7 @@ struct LevelDev {
   double2* pk = nullptr;
   double* gy = nullptr;
   double *img = nullptr, *illum = nullptr, *base = nullptr, *delta = nullptr, *total = nullptr;
-  double *nodew = nullptr, *half = nullptr, *cells = nullptr, *sys = nullptr, *xa = nullptr, *xb = nullptr,
+  double *nodew = nullptr, *nodew2 = nullptr, *nodew_a = nullptr, *nodew_b = nullptr, *half = nullptr, *cells = nullptr, *sys = nullptr, *xa = nullptr, *xb = nullptr,
          *hm = nullptr;
   uint8_t *vis = nullptr, *W = nullptr, *occ = nullptr;
   int n_pix_cta = 0, n_node_cta = 0;
@@ -104,7 +104,8 @@ struct LevelDev {
     base = m.alloc<double>(B * G * 6);
     delta = m.alloc<double>(B * G * 6);
     total = m.alloc<double>(B * G * 6);
-    nodew = m.alloc<double>(B * G);
+    nodew_a = nodew = m.alloc<double>(B * G);
+    nodew_b = nodew2 = m.alloc<double>(B * G);
     half = m.alloc<double>(B * N);
     cells = m.alloc<double>(B * C * kCellStride);
     sys = m.alloc<double>(B * G * kSysStride);
@@ -185,7 +186,8 @@ inline void record_gn_level(LevelDev& d, int B, const hwf_energy_params& P, cons
   pa.active = S.active_fields; pa.refresh = 1;
   NodeArgs na{};
   na.w = d.w; na.h = d.h; na.gw = d.gw; na.gh = d.gh; na.step = d.step; na.ncx = d.ncx; na.ncy = d.ncy;
-  na.half = d.half; na.node_w = d.nodew; na.total = d.total; na.delta = d.delta; na.cells = d.cells;
+  na.half = d.half; na.node_w = d.nodew; na.node_w_new = d.nodew; na.total = d.total; na.delta = d.delta;
+  na.cells = d.cells;
   na.sys = d.sys; na.ep_pair = E.pair_stride(); na.ep_base = d.n_pix_cta; na.flags = flags;
   na.P = to_params(P); na.F = dF; na.active = S.active_fields; na.lm = S.lm_lambda; na.refresh = 1;
   for (int it = 0; it < gn; ++it) {
@@ -197,10 +199,16 @@ inline void record_gn_level(LevelDev& d, int B, const hwf_energy_params& P, cons
       CK(cudaEventRecordWithFlags((*L.ev)[2 * L.bytes->size() + 1], st, cudaEventRecordExternal));
       L.bytes->push_back(pixel_bytes(d, B, d.illum != nullptr));
     }
+    // w_i refresh into the other buffer; the old one still serves E_after(it-1)
+    double* wnew = d.nodew == d.nodew_a ? d.nodew_b : d.nodew_a;
+    launch_structw(d.w, d.h, d.gw, d.gh, d.step, d.half, wnew, B, st);
+    na.node_w = d.nodew;
+    na.node_w_new = wnew;
     na.ep_new = pa.ep_new;
     na.ep_old = pa.ep_old;
     launch_node(true, na, B, st);
-    L.count += 2;
+    d.nodew = wnew;
+    L.count += 3;
     if (S.subdomain_px > 0) {
       SwzArgs sa{};
       sa.gw = d.gw; sa.gh = d.gh; sa.step = d.step; sa.tile = d.tile; sa.ntx = d.ntx; sa.nty = d.nty;
@@ -229,6 +237,8 @@ inline void record_gn_level(LevelDev& d, int B, const hwf_energy_params& P, cons
     pa.ep_old = nullptr;
     launch_pixel(false, pa, B, st);
     na.refresh = 0;
+    na.node_w = d.nodew;
+    na.node_w_new = d.nodew;
     na.ep_new = pa.ep_new;
     na.ep_old = nullptr;
     launch_node(false, na, B, st);

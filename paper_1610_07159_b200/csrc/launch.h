@@ -38,8 +38,9 @@ struct PixArgs {
 
 struct NodeArgs {
   int w, h, gw, gh, step, ncx, ncy;
-  const double* half;   // [B][N]
-  double* node_w;       // [B][G]
+  const double* half;        // [B][N]
+  const double* node_w;      // [B][G] w_i of the previous iteration (E_after of it-1)
+  const double* node_w_new;  // [B][G] refreshed w_i (k_structw), == node_w when refresh = 0
   const double* total;  // [B][G][6]
   const double* delta;  // [B][G][6]
   const double* cells;  // [B][C][234]
@@ -96,6 +97,8 @@ void launch_pixel(bool lin, const PixArgs& a, int B, cudaStream_t s);
 void launch_pack(const double* img, int w, int h, int planes, double2* pk, double* gy, cudaStream_t s);
 int node_ctas(int G);
 void launch_node(bool lin, const NodeArgs& a, int B, cudaStream_t s);
+void launch_structw(int w, int h, int gw, int gh, int step, const double* half, double* wout, int B,
+                    cudaStream_t s);
 
 // solve.cu
 void launch_schwarz(const SwzArgs& a, int B, cudaStream_t s);

@@ -83,7 +83,8 @@ NodeArgs node_args(const LevelDev& d, const hwf_energy_params* P, uint32_t activ
                    int* flags, const Energies& E) {
   NodeArgs na{};
   na.w = d.w; na.h = d.h; na.gw = d.gw; na.gh = d.gh; na.step = d.step; na.ncx = d.ncx; na.ncy = d.ncy;
-  na.half = d.half; na.node_w = d.nodew; na.total = d.total; na.delta = d.delta; na.cells = d.cells;
+  na.half = d.half; na.node_w = d.nodew; na.node_w_new = d.nodew; na.total = d.total; na.delta = d.delta;
+  na.cells = d.cells;
   na.sys = d.sys; na.ep_pair = E.pair_stride(); na.ep_base = d.n_pix_cta; na.flags = flags;
   na.P = to_params(*P); na.F = dF; na.active = active; na.lm = lm; na.ep_new = E.slot(0);
   return na;
@@ -239,13 +240,11 @@ int hwf_refresh_weights(hwf_ctx* ctx, const hwf_level* lv, const hwf_energy_para
     PixArgs pa = pix_args(d, P, 7u, flags, E);
     pa.refresh = 1;
     launch_pixel(true, pa, 1, ctx->stream);
-    NodeArgs na = node_args(d, P, 7u, 0.0, dF, flags, E);
-    na.refresh = 1;
-    launch_node(true, na, 1, ctx->stream);
+    launch_structw(d.w, d.h, d.gw, d.gh, d.step, d.half, d.nodew2, 1, ctx->stream);
     CK(cudaStreamSynchronize(ctx->stream));
     CK(cudaGetLastError());
     if (outlier_out) down(outlier_out, d.W, d.N);
-    if (node_w_out) down(node_w_out, d.nodew, d.G);
+    if (node_w_out) down(node_w_out, d.nodew2, d.G);
   });
 }
 

@@ -30,8 +30,18 @@ def _octave(rng: np.random.Generator, spacing: float, xs: np.ndarray, ys: np.nda
     return a * (1 - fv) + b * fv
 
 
+def _weights_1d(coord: np.ndarray, spacing: float, n: int):
+    """Lattice cell and smoothstep weight along one axis (same rule as _octave)."""
+    u = coord / spacing + 2.0
+    i = np.clip(np.floor(u).astype(np.int64), 0, n - 2)
+    f = np.clip(u - i, 0.0, 1.0)
+    return i, f * f * (3 - 2 * f)
+
+
 class Texture:
     """Continuous, seeded texture T(x, y) over a margin-padded domain."""
+
+    SPACINGS = (4.0, 8.0, 16.0, 32.0)
 
     def __init__(self, seed: int, w: int, h: int, margin: int = 96):
         self.seed, self.margin = seed, margin
@@ -41,8 +51,25 @@ class Texture:
         rng = np.random.default_rng(self.seed)
         X, Y = xs + self.margin, ys + self.margin
         t = np.zeros_like(X, dtype=np.float64)
-        for k, sp in enumerate((4.0, 8.0, 16.0, 32.0)):
+        for k, sp in enumerate(self.SPACINGS):
             t += (0.5 ** (3 - k)) * _octave(rng, sp, X, Y, self.extent)
+        t /= 1.875
+        return 0.1 + 0.8 * np.clip(t, 0.0, 1.0)
+
+    def grid(self, x: np.ndarray, y: np.ndarray) -> np.ndarray:
+        """T on the separable grid (y[r], x[c]); same values as __call__ on that grid,
+        evaluated per octave as a 1-D blend along x for every lattice row, then along y."""
+        rng = np.random.default_rng(self.seed)
+        X, Y = x + self.margin, y + self.margin
+        t = np.zeros((y.size, x.size))
+        for k, sp in enumerate(self.SPACINGS):
+            gx = int(np.ceil(self.extent[0] / sp)) + 4
+            gy = int(np.ceil(self.extent[1] / sp)) + 4
+            lat = rng.random((gy, gx))
+            i, fu = _weights_1d(X, sp, gx)
+            j, fv = _weights_1d(Y, sp, gy)
+            A = lat[:, i] * (1 - fu) + lat[:, i + 1] * fu  # (gy, W)
+            t += (0.5 ** (3 - k)) * (A[j] * (1 - fv)[:, None] + A[j + 1] * fv[:, None])
         t /= 1.875
         return 0.1 + 0.8 * np.clip(t, 0.0, 1.0)
 
@@ -57,22 +84,21 @@ def render_pair(w: int, h: int, s=(0.0, 0.0), m=(0.0, 0.0), d=(0.0, 0.0), seed: 
     """
     T = Texture(seed, w, h)
     Tf = Texture(seed + 7919, w, h) if occluder else None
-    yy, xx = np.mgrid[0:h, 0:w].astype(np.float64)
+    x1d, y1d = np.arange(w, dtype=np.float64), np.arange(h, dtype=np.float64)
     rng = np.random.default_rng(seed + 1)
     out = np.empty((4, h, w))
     for e in range(4):
         sc = -1.0 if (e & 1) == 0 else 1.0
         st = -1.0 if (e >> 1) == 0 else 1.0
-        bx = xx - sc * s[0] - st * m[0] - sc * st * d[0]
-        by = yy - sc * s[1] - st * m[1] - sc * st * d[1]
-        img = T(bx, by)
+        # constant flows: the pull-back grid is the pixel grid shifted (separable)
+        img = T.grid(x1d - (sc * s[0] + st * m[0] + sc * st * d[0]), y1d - (sc * s[1] + st * m[1] + sc * st * d[1]))
         if occluder:
             x0, y0, x1, y1 = occluder["rect"]
             fs = (s[0] + occluder["extra_s"][0], s[1] + occluder["extra_s"][1])
-            fx = xx - sc * fs[0] - st * m[0] - sc * st * d[0]
-            fy = yy - sc * fs[1] - st * m[1] - sc * st * d[1]
-            inside = (fx >= x0) & (fx < x1) & (fy >= y0) & (fy < y1)
-            img = np.where(inside, Tf(fx, fy), img)
+            fx = x1d - (sc * fs[0] + st * m[0] + sc * st * d[0])
+            fy = y1d - (sc * fs[1] + st * m[1] + sc * st * d[1])
+            inside = ((fy >= y0) & (fy < y1))[:, None] & ((fx >= x0) & (fx < x1))[None, :]
+            img = np.where(inside, Tf.grid(fx, fy), img)
         if gain_offset:
             img = img * gain_offset.get("gain", [1, 1, 1, 1])[e] + gain_offset.get("offset", [0, 0, 0, 0])[e]
         img = img + noise * rng.standard_normal(img.shape)
@@ -94,3 +120,25 @@ def constant_pair(w: int = 320, h: int = 240, seed: int = 1610) -> tuple[np.ndar
     """cfg1: s = (1.5, 0) (disparity 3 px), m = (0.75, 0.5) (motion (1.5, 1.0)), d = 0."""
     s, m = (1.5, 0.0), (0.75, 0.5)
     return render_pair(w, h, s=s, m=m, seed=seed), {"s": s, "m": m, "d": (0.0, 0.0)}
+
+
+def valgaerts_pair(index: int = 0, w: int = 1920, h: int = 1080) -> tuple[np.ndarray, dict]:
+    """cfg3: two-layer occluder (foreground square with +6 px extra disparity, i.e. +3 px
+    of half-disparity s) and per-camera illumination change (right camera +0.05 offset,
+    t+1 gain x1.05), SURVEY.md §8d."""
+    rng = np.random.default_rng(7919 + index)
+    s = (float(rng.uniform(1.0, 3.0)), 0.0)
+    m = (float(rng.uniform(-1.5, 1.5)), float(rng.uniform(-1.0, 1.0)))
+    rect = (w // 3, h // 3, 2 * w // 3, 2 * h // 3)
+    go = {"offset": [0.0, 0.05, 0.0, 0.05], "gain": [1.0, 1.0, 1.05, 1.05]}
+    imgs = render_pair(w, h, s=s, m=m, seed=2000 + index, occluder={"rect": rect, "extra_s": (3.0, 0.0)},
+                       gain_offset=go)
+    return imgs, {"s": s, "m": m, "d": (0.0, 0.0), "rect": rect, "extra_s": (3.0, 0.0)}
+
+
+def uhd_pair(index: int = 0, w: int = 3840, h: int = 2160) -> tuple[np.ndarray, dict]:
+    """cfg5: one 3840x2160 pair with known constant flow."""
+    rng = np.random.default_rng(4000 + index)
+    s = (float(rng.uniform(1.0, 6.0)), 0.0)
+    m = (float(rng.uniform(-3.0, 3.0)), float(rng.uniform(-3.0, 3.0)))
+    return render_pair(w, h, s=s, m=m, seed=4000 + index), {"s": s, "m": m, "d": (0.0, 0.0)}

@@ -267,3 +267,21 @@ def test_divergence_is_reported(device):
         pass  # reported, not aborted
     with pytest.raises(ValueError):
         device.solve_batch(imgs[None], EnergyParams.preset("facial"), S)  # w_epi > 0 without F
+
+
+# ---- the other BASELINE.json shapes ----------------------------------------------
+def test_cfg3_occluder_and_illumination_change(device, oracle):
+    """cfg3: 1920x1080, 5 levels, foreground square with +6 px extra disparity, right camera +0.05,
+    t+1 gain x1.05 (short GN schedule so the CPU oracle stays fast)."""
+    imgs, gt = synthetic.valgaerts_pair(0)
+    S = SolveSchedule(levels=5, grid_step=8, gn_per_level=[1, 1, 2], pcg_iters=5, patch_iters=5, threads=16)
+    r, s = _check_solve(device, oracle, imgs, EnergyParams(), S)
+    assert (r.vis4 != 0x0F).any()  # the occluder produces occlusion
+    assert np.isfinite(r.grid_total).all()
+
+
+def test_cfg5_uhd_step4_general_schwarz_tiles(device, oracle):
+    """cfg5: 3840x2160, 4 px grid -> 4x4-node subdomains (the general Schwarz team path)."""
+    imgs, _ = synthetic.uhd_pair(0)
+    S = SolveSchedule(levels=5, grid_step=4, gn_per_level=[1], pcg_iters=5, patch_iters=3, threads=16)
+    _check_solve(device, oracle, imgs, EnergyParams(), S)
