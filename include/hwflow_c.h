@@ -22,6 +22,7 @@
  *   hwf_occlusion      -> compute_occlusion_maps  SPEC.md:414-422 (no code shipped)
  *   hwf_illumination   -> compute_illumination_maps SPEC.md:423-431 (no code shipped)
  *   hwf_prolongate     -> prolongate              SPEC.md:405-413 (no code shipped)
+ *   hwf_propagate_temporal / hwf_solve_batch_seq -> propagate_temporal SPEC.md:432-440 (no code shipped)
  *
  * Error convention (replaces the exceptions of the reference):
  *   HWF_OK 0, HWF_EINVAL 1 (std::invalid_argument / std::out_of_range),
@@ -157,6 +158,26 @@ int hwf_solve_batch(hwf_ctx* ctx, int n_pairs, const hwf_frame4* frames,
                     const hwf_energy_params* params, const hwf_schedule* sched,
                     const double* fundamental, hwf_result* out /*n_pairs*/,
                     hwf_stats* stats /*n_pairs, nullable*/);
+
+/* ---- sequences: temporal propagation ------------------- */
+/* Opaque per-level solver state of n frame pairs (the delta hierarchy and the
+ * accumulated grids), device-resident in the CUDA library. */
+typedef struct hwf_state hwf_state;
+int hwf_state_create(hwf_ctx* ctx, int n_pairs, int width, int height, int levels, int grid_step,
+                     hwf_state** out);
+void hwf_state_destroy(hwf_state* st);
+/* Finest-to-coarsest copy-out of one pair's state: delta and total, 6G_l each, level-major. */
+int hwf_state_read(hwf_ctx* ctx, const hwf_state* st, int pair, double* delta, double* total);
+/* Like hwf_solve_batch, but each level's delta starts from the previous frame's
+ * delta advected along its motion (prev nullable: first frame, zero deltas), and
+ * the solved hierarchy is written to next (nullable). SPEC.md:396-404, 432-440. */
+int hwf_solve_batch_seq(hwf_ctx* ctx, int n_pairs, const hwf_frame4* frames,
+                        const hwf_energy_params* params, const hwf_schedule* sched,
+                        const double* fundamental, const hwf_state* prev, hwf_state* next,
+                        hwf_result* out, hwf_stats* stats);
+/* propagate_temporal for one level: next_delta(p) = prev_delta(p - 2 m_prev(p)), zero outside. */
+int hwf_propagate_temporal(hwf_ctx* ctx, int width, int height, int grid_step, const double* prev_delta,
+                           const double* prev_total, double* next_delta);
 
 /* ---- per-stage entry points (parity seams) ------------------------------ */
 /* out: for l in levels, for e in 0..3: h_l*w_l doubles (level 0 = finest). */

@@ -41,6 +41,13 @@ struct hwf_ctx {
   std::string err;
 };
 
+// Per-pair delta hierarchy + accumulated grids (SPEC.md:396 `prev`).
+struct hwf_state {
+  int n = 0, w = 0, h = 0, L = 0, step = 0;
+  bool valid = false;
+  std::vector<std::vector<std::vector<double>>> delta, total;  // [pair][level][6G]
+};
+
 namespace orc {
 namespace {
 
@@ -240,6 +247,23 @@ void prolongate(int wc, int hc, int wf, int hf, int step, const double* total_c,
   }
 }
 
+// ---- temporal propagation (pin: pull-back along the previous
+// frame's accumulated motion at the node, p - 2 m(p), bilinear WarpGrid sample of
+// the previous delta, all six components zero outside the lattice coverage)
+void propagate(int w, int h, int step, const double* prev_delta, const double* prev_total, double* next_delta) {
+  const GridDims g = grid_dims(w, h, step);
+  const double xmax = static_cast<double>(g.gw - 1) * step, ymax = static_cast<double>(g.gh - 1) * step;
+  for (int k = 0; k < g.nodes(); ++k) {
+    const double px = static_cast<double>((k % g.gw) * step), py = static_cast<double>((k / g.gw) * step);
+    const double qx = px - 2.0 * prev_total[6 * k + 2], qy = py - 2.0 * prev_total[6 * k + 3];
+    if (qx >= 0.0 && qy >= 0.0 && qx <= xmax && qy <= ymax) {
+      interpolate(g, prev_delta, qx, qy, next_delta + 6 * k);
+    } else {
+      for (int c = 0; c < 6; ++c) next_delta[6 * k + c] = 0.0;
+    }
+  }
+}
+
 namespace {
 
 int gn_for_level(const hwf_schedule* S, int l) {  // solver.hpp:30-34
@@ -249,7 +273,8 @@ int gn_for_level(const hwf_schedule* S, int l) {  // solver.hpp:30-34
 
 // Algorithm 1.
 void run_scene_flow(Backend* B, const hwf_frame4* fr, const hwf_energy_params* P,
-                    const hwf_schedule* S, const double* F, hwf_result* out, hwf_stats* stats) {
+                    const hwf_schedule* S, const double* F, hwf_result* out, hwf_stats* stats,
+                    const hwf_state* prev = nullptr, hwf_state* next = nullptr, int pair = 0) {
   if (hwf_validate_params(P) != HWF_OK) throw std::invalid_argument("energy weights must be >= 0");
   if (P->w_epi > 0.0 && !F) throw std::invalid_argument("epipolar term enabled without a fundamental matrix");
   const auto imgs = load_frames(fr);
@@ -273,6 +298,8 @@ void run_scene_flow(Backend* B, const hwf_frame4* fr, const hwf_energy_params* P
     const int w = dims[4 * l], h = dims[4 * l + 1], N = w * h;
     const int G = dims[4 * l + 2] * dims[4 * l + 3];
     std::vector<double> base(6 * static_cast<size_t>(G), 0.0), delta(6 * static_cast<size_t>(G), 0.0);
+    if (prev && prev->valid)  // warm start; first frame: zero deltas
+      propagate(w, h, S->grid_step, prev->delta[pair][l].data(), prev->total[pair][l].data(), delta.data());
     std::vector<uint8_t> vis(N, 0x0F), outl(N, 1);
     std::vector<double> node_w(G, 1.0), hm;
     if (l == L - 1) {
@@ -299,7 +326,7 @@ void run_scene_flow(Backend* B, const hwf_frame4* fr, const hwf_energy_params* P
         lv.illum[e] = illum.data() + static_cast<size_t>(e) * N;
       }
     }
-    lv.total = base.data();
+    lv.total = base.data();  // rebound inside gauss_newton to base + delta
     lv.delta = delta.data();
     lv.vis4 = vis.data();
     lv.outlier = outl.data();
@@ -317,6 +344,10 @@ void run_scene_flow(Backend* B, const hwf_frame4* fr, const hwf_energy_params* P
     }
     std::vector<double> total(base.size());
     for (size_t i = 0; i < total.size(); ++i) total[i] = base[i] + delta[i];
+    if (next) {
+      next->delta[pair][l] = delta;
+      next->total[pair][l] = total;
+    }
     std::vector<uint8_t> vis_new(N);
     occlusion(w, h, S->grid_step, total.data(), vis_new.data());
     if (l > 0) {
@@ -446,6 +477,60 @@ int hwf_solve_batch(hwf_ctx* ctx, int n, const hwf_frame4* frames, const hwf_ene
   }
   return HWF_OK;
 }
+int hwf_state_create(hwf_ctx* ctx, int n, int w, int h, int levels, int step, hwf_state** out) {
+  return orc::guard(ctx, [&] {
+    int L = 0, dims[4 * HWF_MAX_LEVELS];
+    if (n < 1 || hwf_level_dims(w, h, levels, step, &L, dims) != HWF_OK) throw std::invalid_argument("bad state dims");
+    auto* st = new hwf_state();
+    st->n = n;
+    st->w = w;
+    st->h = h;
+    st->L = L;
+    st->step = step;
+    st->delta.assign(n, std::vector<std::vector<double>>(L));
+    st->total.assign(n, std::vector<std::vector<double>>(L));
+    for (int i = 0; i < n; ++i)
+      for (int l = 0; l < L; ++l) {
+        st->delta[i][l].assign(6ull * dims[4 * l + 2] * dims[4 * l + 3], 0.0);
+        st->total[i][l].assign(6ull * dims[4 * l + 2] * dims[4 * l + 3], 0.0);
+      }
+    *out = st;
+  });
+}
+void hwf_state_destroy(hwf_state* st) { delete st; }
+int hwf_state_read(hwf_ctx* ctx, const hwf_state* st, int pair, double* delta, double* total) {
+  return orc::guard(ctx, [&] {
+    if (!st || pair < 0 || pair >= st->n) throw std::invalid_argument("bad state/pair");
+    size_t off = 0;
+    for (int l = 0; l < st->L; ++l) {
+      const auto& d = st->delta[pair][l];
+      if (delta) std::memcpy(delta + off, d.data(), d.size() * sizeof(double));
+      if (total) std::memcpy(total + off, st->total[pair][l].data(), d.size() * sizeof(double));
+      off += d.size();
+    }
+  });
+}
+int hwf_solve_batch_seq(hwf_ctx* ctx, int n, const hwf_frame4* frames, const hwf_energy_params* params,
+                        const hwf_schedule* sched, const double* F, const hwf_state* prev, hwf_state* next,
+                        hwf_result* out, hwf_stats* stats) {
+  return orc::guard(ctx, [&] {
+    int L = 0, dims[4 * HWF_MAX_LEVELS];
+    if (hwf_level_dims(frames[0].width, frames[0].height, sched->levels, sched->grid_step, &L, dims) != HWF_OK)
+      throw std::invalid_argument("bad dims");
+    for (const hwf_state* st : {prev, static_cast<const hwf_state*>(next)})
+      if (st && (st->n != n || st->w != frames[0].width || st->h != frames[0].height || st->L != L ||
+                 st->step != sched->grid_step))
+        throw std::invalid_argument("state does not match the batch (pairs, size, levels, grid step)");
+    for (int i = 0; i < n; ++i)
+      orc::run_scene_flow(orc::backend(), frames + i, params, sched, F, out + i, stats ? stats + i : nullptr, prev,
+                          next, i);
+    if (next) next->valid = true;
+  });
+}
+int hwf_propagate_temporal(hwf_ctx* ctx, int w, int h, int step, const double* pd, const double* pt, double* nd) {
+  return orc::guard(ctx, [&] { orc::propagate(w, h, step, pd, pt, nd); });
+}
+
 int hwf_pyramid(hwf_ctx* ctx, const hwf_frame4* frames, int levels, double* out) {
   return orc::guard(ctx, [&] {
     if (levels < 1) throw std::invalid_argument("pyramid needs >= 1 level");

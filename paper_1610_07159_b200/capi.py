@@ -102,6 +102,13 @@ _SIGS = {
                                  _dp, C.POINTER(ResultC), C.POINTER(StatsC)]),
     "hwf_solve_batch": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(Frame4C), C.POINTER(EnergyParamsC),
                                   C.POINTER(ScheduleC), _dp, C.POINTER(ResultC), C.POINTER(StatsC)]),
+    "hwf_state_create": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "hwf_state_destroy": (None, [C.c_void_p]),
+    "hwf_state_read": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, _dp, _dp]),
+    "hwf_solve_batch_seq": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(Frame4C), C.POINTER(EnergyParamsC),
+                                      C.POINTER(ScheduleC), _dp, C.c_void_p, C.c_void_p, C.POINTER(ResultC),
+                                      C.POINTER(StatsC)]),
+    "hwf_propagate_temporal": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp]),
     "hwf_pyramid": (C.c_int, [C.c_void_p, C.POINTER(Frame4C), C.c_int, _dp]),
     "hwf_eval_energy": (C.c_int, [C.c_void_p, C.POINTER(LevelC), C.POINTER(EnergyParamsC), C.POINTER(EnergyC), _dp]),
     "hwf_refresh_weights": (C.c_int, [C.c_void_p, C.POINTER(LevelC), C.POINTER(EnergyParamsC), _u8p, _dp]),

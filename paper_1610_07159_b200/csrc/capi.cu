@@ -160,6 +160,99 @@ int hwf_solve_batch(hwf_ctx* ctx, int n, const hwf_frame4* frames, const hwf_ene
   });
 }
 
+// ---- sequences (temporal propagation) ---------------------------------------------
+int hwf_state_create(hwf_ctx* ctx, int n, int w, int h, int levels, int step, hwf_state** out) {
+  return guard(ctx, [&] {
+    int L = 0, dims[4 * HWF_MAX_LEVELS];
+    if (!out || n < 1 || hwf_level_dims(w, h, levels, step, &L, dims) != HWF_OK) throw InvalidArg("bad state dims");
+    auto st = std::make_unique<hwf_state>();
+    st->device = ctx->device;
+    st->n = n;
+    st->w = w;
+    st->h = h;
+    st->L = L;
+    st->step = step;
+    for (int l = 0; l < L; ++l) {
+      st->G[l] = static_cast<size_t>(dims[4 * l + 2]) * dims[4 * l + 3];
+      CK(cudaMalloc(&st->delta[l], sizeof(double) * 6 * n * st->G[l]));
+      CK(cudaMalloc(&st->total[l], sizeof(double) * 6 * n * st->G[l]));
+      CK(cudaMemset(st->delta[l], 0, sizeof(double) * 6 * n * st->G[l]));
+      CK(cudaMemset(st->total[l], 0, sizeof(double) * 6 * n * st->G[l]));
+    }
+    *out = st.release();
+  });
+}
+void hwf_state_destroy(hwf_state* st) { delete st; }
+int hwf_state_read(hwf_ctx* ctx, const hwf_state* st, int pair, double* delta, double* total) {
+  return guard(ctx, [&] {
+    if (!st || pair < 0 || pair >= st->n) throw InvalidArg("bad state/pair");
+    size_t off = 0;
+    for (int l = 0; l < st->L; ++l) {
+      const size_t m = 6 * st->G[l];
+      if (delta) CK(cudaMemcpy(delta + off, st->delta[l] + pair * m, m * sizeof(double), cudaMemcpyDeviceToHost));
+      if (total) CK(cudaMemcpy(total + off, st->total[l] + pair * m, m * sizeof(double), cudaMemcpyDeviceToHost));
+      off += m;
+    }
+  });
+}
+
+int hwf_solve_batch_seq(hwf_ctx* ctx, int n, const hwf_frame4* frames, const hwf_energy_params* params,
+                        const hwf_schedule* sched, const double* F, const hwf_state* prev, hwf_state* next,
+                        hwf_result* out, hwf_stats* stats) {
+  return guard(ctx, [&] {
+    if (n < 1 || !frames || !out) throw InvalidArg("bad batch");
+    check_params(params, sched, F);
+    const int w = frames[0].width, h = frames[0].height, dt = frames[0].dtype;
+    int L = 0, dims[4 * HWF_MAX_LEVELS];
+    if (hwf_level_dims(w, h, sched->levels, sched->grid_step, &L, dims) != HWF_OK) throw InvalidArg("bad dims");
+    for (const hwf_state* st : {prev, static_cast<const hwf_state*>(next)})
+      if (st && (st->n != n || st->w != w || st->h != h || st->L != L || st->step != sched->grid_step))
+        throw InvalidArg("state does not match the batch (pairs, size, levels, grid step)");
+    for (int i = 0; i < n; ++i) {
+      if (frames[i].width != w || frames[i].height != h || frames[i].dtype != dt)
+        throw InvalidArg("all pairs of a batch must share size and dtype");
+      for (int e = 0; e < 4; ++e)
+        if (!frames[i].plane[e]) throw InvalidArg("null image plane");
+    }
+    unsigned om = 0;
+    for (int i = 0; i < n; ++i)
+      om |= (out[i].s ? 1u : 0u) | (out[i].m ? 2u : 0u) | (out[i].d ? 4u : 0u) | (out[i].disparity ? 8u : 0u);
+    const bool use_prev = prev && prev->valid;
+    Plan& p = get_plan(ctx, n, w, h, dt, params, sched, F, om, use_prev);
+    cudaStream_t st = ctx->stream;
+    if (use_prev)
+      for (int l = 0; l < L; ++l) {
+        const size_t m = sizeof(double) * 6 * n * p.lv[l].G;
+        CK(cudaMemcpyAsync(p.prev_delta[l], prev->delta[l], m, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(p.prev_total[l], prev->total[l], m, cudaMemcpyDeviceToDevice, st));
+      }
+    upload_frames(p, n, frames, st);
+    CK(cudaGraphLaunch(p.exec, st));
+    if (next)
+      for (int l = 0; l < L; ++l) {
+        const size_t m = sizeof(double) * 6 * n * p.lv[l].G;
+        CK(cudaMemcpyAsync(next->delta[l], p.lv[l].delta, m, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(next->total[l], p.lv[l].total, m, cudaMemcpyDeviceToDevice, st));
+      }
+    const size_t N = p.lv[0].N, G = p.lv[0].G;
+    for (int i = 0; i < n; ++i) {
+      const hwf_result& r = out[i];
+      if (r.s) CK(cudaMemcpyAsync(r.s, p.o_s + i * N * 2, N * 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+      if (r.m) CK(cudaMemcpyAsync(r.m, p.o_m + i * N * 2, N * 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+      if (r.d) CK(cudaMemcpyAsync(r.d, p.o_d + i * N * 2, N * 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+      if (r.disparity) CK(cudaMemcpyAsync(r.disparity, p.o_disp + i * N, N * sizeof(double), cudaMemcpyDeviceToHost, st));
+      if (r.vis4) CK(cudaMemcpyAsync(r.vis4, p.lv[0].occ + i * N, N, cudaMemcpyDeviceToHost, st));
+      if (r.grid_total)
+        CK(cudaMemcpyAsync(r.grid_total, p.lv[0].total + i * G * 6, G * 6 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    if (next) next->valid = true;
+    std::vector<int> flags;
+    finish_stats(p, n, stats, flags);
+    raise_on_flags(flags, n);
+  });
+}
+
 int hwf_solve_pair(hwf_ctx* ctx, const hwf_frame4* frames, const hwf_energy_params* params,
                    const hwf_schedule* sched, const double* F, hwf_result* out, hwf_stats* stats) {
   return hwf_solve_batch(ctx, 1, frames, params, sched, F, out, stats);

@@ -255,6 +255,9 @@ struct Plan {
   double F[9] = {};
   unsigned outmask = 0;  // 1 s, 2 m, 4 d, 8 disparity
   bool profile = false;
+  bool has_prev = false;  // temporal propagation from a previous frame's state
+  double* prev_delta[HWF_MAX_LEVELS] = {};
+  double* prev_total[HWF_MAX_LEVELS] = {};
 
   int L = 0;
   LevelDev lv[HWF_MAX_LEVELS];
@@ -274,8 +277,9 @@ struct Plan {
   std::vector<double> ev_bytes;
 
   bool matches(int B_, int w_, int h_, int dt, const hwf_energy_params& P_, const hwf_schedule& S_, const double* F_,
-               unsigned om, bool prof) const {
-    if (B != B_ || w != w_ || h != h_ || dtype != dt || outmask != om || profile != prof) return false;
+               unsigned om, bool prof, bool prev) const {
+    if (B != B_ || w != w_ || h != h_ || dtype != dt || outmask != om || profile != prof || has_prev != prev)
+      return false;
     if (std::memcmp(&P, &P_, sizeof(P)) || std::memcmp(&S, &S_, sizeof(S))) return false;
     if (hasF != (F_ != nullptr)) return false;
     return !F_ || std::memcmp(F, F_, sizeof(F)) == 0;
@@ -310,6 +314,10 @@ struct Plan {
       d.alloc_solver(mem, B, S.subdomain_px > 0);
       d.occ = mem.alloc<uint8_t>(B * d.N);
       if (l < L - 1) d.illum = mem.alloc<double>(B * 4 * d.N);
+      if (has_prev) {
+        prev_delta[l] = mem.alloc<double>(B * d.G * 6);
+        prev_total[l] = mem.alloc<double>(B * d.G * 6);
+      }
       if (l > 0) d.hm = mem.alloc<double>(B * 2 * d.N);
     }
     sc.alloc(mem, B, N0, lv[0].G, true, L > 1, S.subdomain_px <= 0);
@@ -379,6 +387,10 @@ struct Plan {
         launch_prolong_maps(c.w, c.h, d.w, d.h, c.occ, c.hm, d.vis, d.illum, B, st);
         LC.count += 2;
       }
+      if (has_prev) {  // warm start: delta_l = advected previous delta
+        launch_propagate(d.gw, d.gh, d.step, prev_delta[l], prev_total[l], d.base, d.delta, d.total, B, st);
+        LC.count++;
+      }
       CK(cudaMemsetAsync(d.W, 1, B * d.N, st));
       CK(cudaMemsetAsync(d.nodew, 0, sizeof(double) * B * d.G, st));
       record_gn_level(d, B, P, S, dF, gn[l], E, slot_base[l], sc, flags, st, LC);
@@ -402,6 +414,22 @@ struct Plan {
 };
 
 }  // namespace hwf_host
+
+// Device-resident per-level state of n pairs (SPEC.md:396 `prev`).
+struct hwf_state {
+  int device = 0, n = 0, w = 0, h = 0, L = 0, step = 0;
+  bool valid = false;
+  size_t G[HWF_MAX_LEVELS] = {};
+  double* delta[HWF_MAX_LEVELS] = {};
+  double* total[HWF_MAX_LEVELS] = {};
+  ~hwf_state() {
+    cudaSetDevice(device);
+    for (int l = 0; l < L; ++l) {
+      if (delta[l]) cudaFree(delta[l]);
+      if (total[l]) cudaFree(total[l]);
+    }
+  }
+};
 
 struct hwf_ctx {
   int device = 0;
@@ -465,8 +493,8 @@ inline void upload_frames(Plan& p, int n, const hwf_frame4* fr, cudaStream_t st)
 }
 
 inline Plan& get_plan(hwf_ctx* ctx, int n, int w, int h, int dtype, const hwf_energy_params* P, const hwf_schedule* S,
-               const double* F, unsigned outmask) {
-  if (ctx->plan && ctx->plan->matches(n, w, h, dtype, *P, *S, F, outmask, ctx->profile)) return *ctx->plan;
+               const double* F, unsigned outmask, bool has_prev = false) {
+  if (ctx->plan && ctx->plan->matches(n, w, h, dtype, *P, *S, F, outmask, ctx->profile, has_prev)) return *ctx->plan;
   ctx->plan.reset();
   CK(cudaStreamSynchronize(ctx->stream));
   auto p = std::make_unique<Plan>();
@@ -480,6 +508,7 @@ inline Plan& get_plan(hwf_ctx* ctx, int n, int w, int h, int dtype, const hwf_en
   if (F) std::memcpy(p->F, F, sizeof(p->F));
   p->outmask = outmask;
   p->profile = ctx->profile;
+  p->has_prev = has_prev;
   p->build(ctx->stream);
   ctx->plan = std::move(p);
   return *ctx->plan;

@@ -120,6 +120,8 @@ void launch_prolong_grid(int gwc, int ghc, int gwf, int ghf, int step, const dou
                          double* base_f, double* total_f, double* delta_f, int B, cudaStream_t s);
 void launch_prolong_maps(int wc, int hc, int wf, int hf, const uint8_t* vis_c, const double* hm_c,
                          uint8_t* vis_f, double* illum_f, int B, cudaStream_t s);
+void launch_propagate(int gw, int gh, int step, const double* prev_delta, const double* prev_total, const double* base,
+                      double* delta, double* total, int B, cudaStream_t s);
 void launch_dense(int w, int h, int gw, int gh, int step, const double* total, int B, double* s_out,
                   double* m_out, double* d_out, double* disp_out, cudaStream_t s);
 void launch_energy_reduce(const double* ep, int nslots, int cap, int B, double* out, int* flags,

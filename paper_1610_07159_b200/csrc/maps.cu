@@ -396,6 +396,27 @@ __global__ void k_prolong_maps(int wc, int hc, int wf, int hf, const uint8_t* __
   }
 }
 
+// ---- temporal propagation (pin in oracle/hierarchy.cpp) ---
+// next_delta(p) = prev_delta(p - 2 m_prev(p)) (exact bilinear, zero outside the
+// lattice); total = base + delta.
+__global__ void k_propagate(int gw, int gh, int step, const double* __restrict__ pd, const double* __restrict__ pt,
+                            const double* __restrict__ base, double* __restrict__ delta, double* __restrict__ total) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x, pair = blockIdx.y;
+  const int G = gw * gh;
+  if (k >= G) return;
+  const size_t o = (static_cast<size_t>(pair) * G + k) * 6;
+  const double px = static_cast<double>((k % gw) * step), py = static_cast<double>((k / gw) * step);
+  const double qx = __dadd_rn(px, -__dmul_rn(2.0, pt[o + 2])), qy = __dadd_rn(py, -__dmul_rn(2.0, pt[o + 3]));
+  const double xmax = static_cast<double>(gw - 1) * step, ymax = static_cast<double>(gh - 1) * step;
+  double fl[6] = {0, 0, 0, 0, 0, 0};
+  if (qx >= 0.0 && qy >= 0.0 && qx <= xmax && qy <= ymax) interp_exact(pd + static_cast<size_t>(pair) * G * 6, gw, gh, step, qx, qy, fl);
+#pragma unroll
+  for (int c = 0; c < 6; ++c) {
+    delta[o + c] = fl[c];
+    if (base) total[o + c] = __dadd_rn(base[o + c], fl[c]);
+  }
+}
+
 // ---- FlowResult (geometry.hpp:26-37) via WarpGrid::interpolate ------------
 __global__ void k_dense(int w, int h, int gw, int gh, int step, const double* __restrict__ total,
                         double* s_out, double* m_out, double* d_out, double* disp_out) {
@@ -493,6 +514,11 @@ void launch_prolong_grid(int gwc, int ghc, int gwf, int ghf, int step, const dou
 void launch_prolong_maps(int wc, int hc, int wf, int hf, const uint8_t* vis_c, const double* hm_c, uint8_t* vis_f,
                          double* illum_f, int B, cudaStream_t s) {
   k_prolong_maps<<<rows_grid(wf, hf, B), kThreads, 0, s>>>(wc, hc, wf, hf, vis_c, hm_c, vis_f, illum_f);
+}
+void launch_propagate(int gw, int gh, int step, const double* prev_delta, const double* prev_total, const double* base,
+                      double* delta, double* total, int B, cudaStream_t s) {
+  k_propagate<<<dim3((gw * gh + kThreads - 1) / kThreads, B), kThreads, 0, s>>>(gw, gh, step, prev_delta, prev_total,
+                                                                               base, delta, total);
 }
 void launch_dense(int w, int h, int gw, int gh, int step, const double* total, int B, double* s_out, double* m_out,
                   double* d_out, double* disp_out, cudaStream_t s) {

@@ -379,6 +379,23 @@ int hwf_gn_level(hwf_ctx* ctx, const hwf_level* lv, const double* base, double* 
   });
 }
 
+int hwf_propagate_temporal(hwf_ctx* ctx, int w, int h, int step, const double* prev_delta, const double* prev_total,
+                           double* next_delta) {
+  return guard(ctx, [&] {
+    if (w < 1 || h < 1 || step < 1) throw InvalidArg("bad dims");
+    DevMem m;
+    LevelDev d;
+    d.dims(w, h, step, 0);
+    const double* pd = up(m, prev_delta, 6 * d.G);
+    const double* pt = up(m, prev_total, 6 * d.G);
+    double* nd = m.alloc<double>(6 * d.G);
+    launch_propagate(d.gw, d.gh, step, pd, pt, nullptr, nd, nullptr, 1, ctx->stream);
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaGetLastError());
+    down(next_delta, nd, 6 * d.G);
+  });
+}
+
 int hwf_occlusion(hwf_ctx* ctx, int w, int h, int step, const double* total, uint8_t* vis4_out) {
   return guard(ctx, [&] {
     if (w < 1 || h < 1 || step < 1) throw InvalidArg("bad dims");

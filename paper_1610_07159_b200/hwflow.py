@@ -211,6 +211,34 @@ def _frame(images: np.ndarray) -> tuple[Frame4C, np.ndarray]:
     return f, a
 
 
+class SequenceState:
+    """hwf_state: the per-level delta hierarchy + accumulated grids of n pairs."""
+
+    def __init__(self, solver: "Solver", n: int, width: int, height: int, schedule: SolveSchedule):
+        self.solver, self.n, self.width, self.height = solver, n, width, height
+        self.levels = level_dims(solver.lib, width, height, schedule.levels, schedule.grid_step)
+        h = C.c_void_p()
+        solver.ctx.check(solver.lib.hwf_state_create(solver.ctx.h, n, width, height, schedule.levels,
+                                                     schedule.grid_step, C.byref(h)))
+        self.h = h
+
+    def read(self, pair: int) -> tuple[list[np.ndarray], list[np.ndarray]]:
+        sizes = [6 * gw * gh for (_, _, gw, gh) in self.levels]
+        d, t = np.empty(sum(sizes)), np.empty(sum(sizes))
+        self.solver.ctx.check(self.solver.lib.hwf_state_read(self.solver.ctx.h, self.h, pair, dptr(d), dptr(t)))
+        offs = np.cumsum([0] + sizes)
+        return ([d[offs[i]:offs[i + 1]].reshape(-1, 6) for i in range(len(sizes))],
+                [t[offs[i]:offs[i + 1]].reshape(-1, 6) for i in range(len(sizes))])
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.solver.lib.hwf_state_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
 class Solver:
     """One device context (or, in tests, one CPU checker) behind the C-ABI."""
 
@@ -235,6 +263,9 @@ class Solver:
                     fundamental: np.ndarray | None = None, outputs=("s", "m", "d", "disparity", "vis4", "grid_total"),
                     ) -> tuple[list[FlowResult], list[GnStats]]:
         """frames: (n, 4, h, w) uint8 or float64 — n independent frame pairs, one device batch."""
+        return self._solve(frames, params, schedule, fundamental, outputs, None, None)
+
+    def _solve(self, frames, params, schedule, fundamental, outputs, prev, nxt):
         a = np.ascontiguousarray(frames)
         if a.ndim != 4 or a.shape[1] != 4:
             raise ValueError("frames must be (n, 4, h, w)")
@@ -264,8 +295,32 @@ class Solver:
         stats = (StatsC * n)()
         F = None if fundamental is None else np.ascontiguousarray(fundamental, np.float64).reshape(9)
         pc, sc = params.to_c(), schedule.to_c()
-        self.ctx.check(self.lib.hwf_solve_batch(self.ctx.h, n, fr, C.byref(pc), C.byref(sc), dptr(F), res, stats))
+        if prev is None and nxt is None:
+            rc = self.lib.hwf_solve_batch(self.ctx.h, n, fr, C.byref(pc), C.byref(sc), dptr(F), res, stats)
+        else:
+            rc = self.lib.hwf_solve_batch_seq(self.ctx.h, n, fr, C.byref(pc), C.byref(sc), dptr(F),
+                                              prev.h if prev is not None else None,
+                                              nxt.h if nxt is not None else None, res, stats)
+        self.ctx.check(rc)
         return outs, [GnStats.from_c(stats[i]) for i in range(n)]
+
+    # ---- sequences: temporal propagation ---------------------
+    def new_state(self, n_pairs: int, width: int, height: int, schedule: SolveSchedule) -> "SequenceState":
+        return SequenceState(self, n_pairs, width, height, schedule)
+
+    def solve_batch_seq(self, frames: np.ndarray, params: EnergyParams, schedule: SolveSchedule,
+                        prev: "SequenceState | None", nxt: "SequenceState | None",
+                        fundamental: np.ndarray | None = None,
+                        outputs=("s", "m", "d", "disparity", "vis4", "grid_total")):
+        """n frame pairs, each warm-started from its own previous frame in `prev` (None: first frame)."""
+        return self._solve(frames, params, schedule, fundamental, outputs, prev, nxt)
+
+    def propagate_temporal(self, width: int, height: int, step: int, prev_delta: np.ndarray,
+                           prev_total: np.ndarray) -> np.ndarray:
+        pd, pt = np.ascontiguousarray(prev_delta, np.float64), np.ascontiguousarray(prev_total, np.float64)
+        out = np.empty_like(pd)
+        self.ctx.check(self.lib.hwf_propagate_temporal(self.ctx.h, width, height, step, dptr(pd), dptr(pt), dptr(out)))
+        return out
 
     def run_scene_flow(self, images: np.ndarray, params: EnergyParams, schedule: SolveSchedule,
                        fundamental: np.ndarray | None = None) -> tuple[FlowResult, GnStats]:

@@ -75,7 +75,8 @@ class Texture:
 
 
 def render_pair(w: int, h: int, s=(0.0, 0.0), m=(0.0, 0.0), d=(0.0, 0.0), seed: int = 1610, noise: float = 0.01,
-                occluder: dict | None = None, gain_offset: dict | None = None, dtype=np.uint8) -> np.ndarray:
+                occluder: dict | None = None, gain_offset: dict | None = None, dtype=np.uint8,
+                shift=(0.0, 0.0)) -> np.ndarray:
     """Four images (4, h, w) by image_index(c,t) = c + 2t for constant flows.
 
     occluder: {"rect": (x0, y0, x1, y1) in the halfway domain, "extra_s": (sx, sy)}
@@ -84,7 +85,8 @@ def render_pair(w: int, h: int, s=(0.0, 0.0), m=(0.0, 0.0), d=(0.0, 0.0), seed: 
     """
     T = Texture(seed, w, h)
     Tf = Texture(seed + 7919, w, h) if occluder else None
-    x1d, y1d = np.arange(w, dtype=np.float64), np.arange(h, dtype=np.float64)
+    # shift: global translation of the scene (sequences: frame k of a moving texture)
+    x1d, y1d = np.arange(w, dtype=np.float64) - shift[0], np.arange(h, dtype=np.float64) - shift[1]
     rng = np.random.default_rng(seed + 1)
     out = np.empty((4, h, w))
     for e in range(4):
@@ -142,3 +144,12 @@ def uhd_pair(index: int = 0, w: int = 3840, h: int = 2160) -> tuple[np.ndarray, 
     s = (float(rng.uniform(1.0, 6.0)), 0.0)
     m = (float(rng.uniform(-3.0, 3.0)), float(rng.uniform(-3.0, 3.0)))
     return render_pair(w, h, s=s, m=m, seed=4000 + index), {"s": s, "m": m, "d": (0.0, 0.0)}
+
+
+def sequence_pairs(n_pairs: int, w: int, h: int, s=(1.5, 0.0), v=(2.0, 1.0), seed: int = 1610) -> list[np.ndarray]:
+    """A constant-velocity stereo sequence: frame t shows the texture translated by t*v (inter-frame
+    motion v = 2m in the halfway convention); pair k = frames (k, k+1), i.e. render_pair with
+    m = v/2 and the scene shifted by (k + 1/2) v. Noise-free so consecutive pairs share pixels."""
+    m = (v[0] / 2.0, v[1] / 2.0)
+    return [render_pair(w, h, s=s, m=m, seed=seed, noise=0.0, shift=((k + 0.5) * v[0], (k + 0.5) * v[1]))
+            for k in range(n_pairs)]

@@ -285,3 +285,38 @@ def test_cfg5_uhd_step4_general_schwarz_tiles(device, oracle):
     imgs, _ = synthetic.uhd_pair(0)
     S = SolveSchedule(levels=5, grid_step=4, gn_per_level=[1], pcg_iters=5, patch_iters=3, threads=16)
     _check_solve(device, oracle, imgs, EnergyParams(), S)
+
+
+# ---- temporal propagation -----------------------------------------
+def test_propagation_bit_exact(device, oracle):
+    rng = np.random.default_rng(5)
+    for (w, h, step) in ((64, 48, 8), (101, 77, 4)):
+        gw, gh = grid_dims(w, h, step)
+        d, t = rng.normal(0, 1, (gw * gh, 6)), rng.normal(0, 3, (gw * gh, 6))
+        assert np.array_equal(device.propagate_temporal(w, h, step, d, t), oracle.propagate_temporal(w, h, step, d, t))
+
+
+def test_sequence_matches_oracle(device, oracle):
+    """Two independent 3-frame sequences advanced together (one device batch per frame)."""
+    seqs = [synthetic.sequence_pairs(3, 128, 96, s=(1.5, 0.0), v=v, seed=1700 + i) for i, v in
+            enumerate(((2.0, 1.0), (-1.0, 0.5)))]
+    # global PCG: the reference's step-8 Schwarz mode diverges (DESIGN.md §2), which would
+    # turn this propagation test into a test of amplified round-off
+    S = SolveSchedule(levels=3, grid_step=8, gn_per_level=[2, 2, 3], pcg_iters=8, subdomain_px=0)
+    P = EnergyParams()
+    dst = [device.new_state(2, 128, 96, S) for _ in range(2)]
+    ost = [[oracle.new_state(1, 128, 96, S) for _ in range(2)] for _ in range(2)]
+    dprev, oprev = None, [None, None]
+    for k in range(3):
+        frames = np.stack([seqs[0][k], seqs[1][k]])
+        ra, sa = device.solve_batch_seq(frames, P, S, dprev, dst[k % 2])
+        dprev = dst[k % 2]
+        for i in range(2):
+            (rb,), (sb,) = oracle.solve_batch_seq(frames[i:i + 1], P, S, oprev[i], ost[i][k % 2])
+            oprev[i] = ost[i][k % 2]
+            assert np.abs(ra[i].grid_total - rb.grid_total).max() < FLOW_TOL_PX
+            np.testing.assert_allclose(sa[i].energy_after[0], sb.energy_after[0], rtol=ENERGY_RTOL)
+            da, ta = dprev.read(i)
+            db, tb = oprev[i].read(0)
+            for l in range(len(da)):
+                assert np.abs(ta[l] - tb[l]).max() < FLOW_TOL_PX

@@ -217,3 +217,35 @@ def test_validation_errors(oracle):
         oracle.run_scene_flow(imgs, bad, SolveSchedule(levels=1, grid_step=8))
     with pytest.raises(ValueError):  # w_epi > 0 without F (energy.cpp:170-171)
         oracle.run_scene_flow(imgs, EnergyParams.preset("facial"), SolveSchedule(levels=1, grid_step=8))
+
+
+# ---- temporal propagation -----------------------------------------
+def test_spec_propagation_examples(oracle):
+    w, h, step = 40, 32, 4
+    gw, gh = grid_dims(w, h, step)
+    rng = np.random.default_rng(0)
+    d = rng.normal(0, 1, (gw * gh, 6))
+    t = np.zeros((gw * gh, 6))
+    np.testing.assert_array_equal(oracle.propagate_temporal(w, h, step, d, t), d)  # zero motion -> identity
+    c = np.tile(np.array([0.3, -0.2, 0.1, 0.4, -0.5, 0.6]), (gw * gh, 1))
+    t[:, 2], t[:, 3] = 0.75, -0.5  # constant motion on constant fields -> unchanged where in coverage
+    out = oracle.propagate_temporal(w, h, step, c, t)
+    a, b = np.arange(gw * gh) % gw, np.arange(gw * gh) // gw
+    inside = (a * step - 1.5 >= 0) & (b * step + 1.0 <= (gh - 1) * step)
+    np.testing.assert_allclose(out[inside], c[inside], rtol=1e-15)
+    assert np.all(out[~inside] == 0.0)  # pulled from outside the lattice -> zero
+
+
+def test_sequence_propagation_lowers_initial_energy(oracle):
+    """SPEC acceptance 12: 3-frame constant-velocity sequence — the initial energy of frame 3
+    with propagation is below the initial energy with zero init."""
+    pairs = synthetic.sequence_pairs(3, 96, 72, s=(1.0, 0.0), v=(2.0, 1.0))
+    S = SolveSchedule(levels=3, grid_step=8, gn_per_level=[2], pcg_iters=8, subdomain_px=0)
+    P = EnergyParams()
+    st = [oracle.new_state(1, 96, 72, S) for _ in range(2)]
+    prev = None
+    for k in range(3):
+        (r,), (s,) = oracle.solve_batch_seq(pairs[k][None], P, S, prev, st[k % 2])
+        prev = st[k % 2]
+    (_,), (cold,) = oracle.solve_batch(pairs[2][None], P, S)
+    assert s.energy_before[0][0] < cold.energy_before[0][0]
