@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -175,70 +176,96 @@ inline double pixel_bytes(const LevelDev& d, int B, bool illum) {
 }
 
 // The nonlinear loop of one level (solver.cpp:484-532) for a batch.
+// Pairs per chunk at a level. A GN iteration can run chunk by chunk (pixel ->
+// structw -> node -> sweeps) so one chunk's cell sums, system and Schwarz vectors
+// stay L2-resident between producer and consumer. Measured on B200 at cfg2,
+// B = 128 (profiles/r1_notes.md): 2/4/8/16/128-pair chunks -> 50.0/46.8/45.1/
+// 44.3/43.9 ms per batch, i.e. the whole batch per launch wins, so that is the
+// default; HWF_CHUNK_L0 (finest level, x4 per coarser level) keeps the knob.
+inline int level_chunk(const LevelDev& d, int B, int level) {
+  (void)d;
+  static const int env = [] {
+    const char* e = std::getenv("HWF_CHUNK_L0");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int c = env > 0 ? env << (2 * level) : B;
+  return std::max(1, std::min(B, c));
+}
+
+// The nonlinear loop of one level (solver.cpp:484-532) for a batch.
 inline void record_gn_level(LevelDev& d, int B, const hwf_energy_params& P, const hwf_schedule& S, const double* dF,
                      int gn, const Energies& E, int slot_base, Scratch& sc, int* flags, cudaStream_t st,
-                     Launches& L) {
-  PixArgs pa{};
-  pa.w = d.w; pa.h = d.h; pa.gw = d.gw; pa.gh = d.gh; pa.step = d.step; pa.ncx = d.ncx; pa.ncy = d.ncy;
-  pa.tcx = d.tcx; pa.tcy = d.tcy; pa.rp = d.rp;
-  pa.pk = d.pk; pa.gy = d.gy; pa.illum = d.illum; pa.vis4 = d.vis; pa.W = d.W; pa.total = d.total; pa.half = d.half;
-  pa.cells = d.cells; pa.ep_pair = E.pair_stride(); pa.flags = flags; pa.P = to_params(P);
-  pa.active = S.active_fields; pa.refresh = 1;
-  NodeArgs na{};
-  na.w = d.w; na.h = d.h; na.gw = d.gw; na.gh = d.gh; na.step = d.step; na.ncx = d.ncx; na.ncy = d.ncy;
-  na.half = d.half; na.node_w = d.nodew; na.node_w_new = d.nodew; na.total = d.total; na.delta = d.delta;
-  na.cells = d.cells;
-  na.sys = d.sys; na.ep_pair = E.pair_stride(); na.ep_base = d.n_pix_cta; na.flags = flags;
-  na.P = to_params(P); na.F = dF; na.active = S.active_fields; na.lm = S.lm_lambda; na.refresh = 1;
+                     Launches& L, int chunk = 0) {
+  const int CH = chunk > 0 ? std::min(chunk, B) : B;
+  const long long eps = E.pair_stride();
   for (int it = 0; it < gn; ++it) {
-    pa.ep_new = E.slot(slot_base + 2 * it);
-    pa.ep_old = it > 0 ? E.slot(slot_base + 2 * (it - 1) + 1) : nullptr;
-    if (L.ev) CK(cudaEventRecordWithFlags((*L.ev)[2 * L.bytes->size()], st, cudaEventRecordExternal));
-    launch_pixel(true, pa, B, st);
-    if (L.ev) {
-      CK(cudaEventRecordWithFlags((*L.ev)[2 * L.bytes->size() + 1], st, cudaEventRecordExternal));
-      L.bytes->push_back(pixel_bytes(d, B, d.illum != nullptr));
-    }
-    // w_i refresh into the other buffer; the old one still serves E_after(it-1)
-    double* wnew = d.nodew == d.nodew_a ? d.nodew_b : d.nodew_a;
-    launch_structw(d.w, d.h, d.gw, d.gh, d.step, d.half, wnew, B, st);
-    na.node_w = d.nodew;
-    na.node_w_new = wnew;
-    na.ep_new = pa.ep_new;
-    na.ep_old = pa.ep_old;
-    launch_node(true, na, B, st);
-    d.nodew = wnew;
-    L.count += 3;
-    if (S.subdomain_px > 0) {
-      SwzArgs sa{};
-      sa.gw = d.gw; sa.gh = d.gh; sa.step = d.step; sa.tile = d.tile; sa.ntx = d.ntx; sa.nty = d.nty;
-      sa.nxm = d.nxm; sa.nym = d.nym; sa.sys = d.sys; sa.delta = d.delta; sa.total = d.total; sa.base = d.base;
-      sa.active = S.active_fields; sa.pcg_iters = S.pcg_iters; sa.flags = flags;
-      for (int s = 0; s < S.patch_iters; ++s) {
-        sa.pub = s == 0 ? nullptr : (s & 1 ? d.xb : d.xa);
-        sa.next = s & 1 ? d.xa : d.xb;
-        sa.last = s == S.patch_iters - 1;
-        launch_schwarz(sa, B, st);
+    double* wnew = d.nodew == d.nodew_a ? d.nodew_b : d.nodew_a;  // ping-pong w_i
+    for (int c0 = 0; c0 < B; c0 += CH) {
+      const int bc = std::min(CH, B - c0);
+      const size_t pN = static_cast<size_t>(c0) * d.N, pG = static_cast<size_t>(c0) * d.G;
+      PixArgs pa{};
+      pa.w = d.w; pa.h = d.h; pa.gw = d.gw; pa.gh = d.gh; pa.step = d.step; pa.ncx = d.ncx; pa.ncy = d.ncy;
+      pa.tcx = d.tcx; pa.tcy = d.tcy; pa.rp = d.rp;
+      pa.pk = d.pk + 4 * pN; pa.gy = d.gy + 4 * pN; pa.illum = d.illum ? d.illum + 4 * pN : nullptr;
+      pa.vis4 = d.vis + pN; pa.W = d.W + pN; pa.total = d.total + 6 * pG; pa.half = d.half + pN;
+      pa.cells = d.cells + static_cast<size_t>(c0) * d.C * kCellStride; pa.ep_pair = eps; pa.flags = flags + c0;
+      pa.P = to_params(P); pa.active = S.active_fields; pa.refresh = 1;
+      pa.ep_new = E.slot(slot_base + 2 * it) + c0 * eps;
+      pa.ep_old = it > 0 ? E.slot(slot_base + 2 * (it - 1) + 1) + c0 * eps : nullptr;
+      if (L.ev) CK(cudaEventRecordWithFlags((*L.ev)[2 * L.bytes->size()], st, cudaEventRecordExternal));
+      launch_pixel(true, pa, bc, st);
+      if (L.ev) {
+        CK(cudaEventRecordWithFlags((*L.ev)[2 * L.bytes->size() + 1], st, cudaEventRecordExternal));
+        L.bytes->push_back(pixel_bytes(d, bc, d.illum != nullptr));
+      }
+      launch_structw(d.w, d.h, d.gw, d.gh, d.step, d.half + pN, wnew + pG, bc, st);
+      NodeArgs na{};
+      na.w = d.w; na.h = d.h; na.gw = d.gw; na.gh = d.gh; na.step = d.step; na.ncx = d.ncx; na.ncy = d.ncy;
+      na.half = d.half + pN; na.node_w = d.nodew + pG; na.node_w_new = wnew + pG; na.total = d.total + 6 * pG;
+      na.delta = d.delta + 6 * pG; na.cells = pa.cells; na.sys = d.sys + static_cast<size_t>(kSysStride) * pG;
+      na.ep_pair = eps; na.ep_base = d.n_pix_cta; na.flags = flags + c0; na.P = to_params(P); na.F = dF;
+      na.active = S.active_fields; na.lm = S.lm_lambda; na.refresh = 1; na.ep_new = pa.ep_new; na.ep_old = pa.ep_old;
+      launch_node(true, na, bc, st);
+      L.count += 3;
+      if (S.subdomain_px > 0) {
+        SwzArgs sa{};
+        sa.gw = d.gw; sa.gh = d.gh; sa.step = d.step; sa.tile = d.tile; sa.ntx = d.ntx; sa.nty = d.nty;
+        sa.nxm = d.nxm; sa.nym = d.nym; sa.sys = na.sys; sa.delta = d.delta + 6 * pG; sa.total = d.total + 6 * pG;
+        sa.base = d.base + 6 * pG; sa.active = S.active_fields; sa.pcg_iters = S.pcg_iters; sa.flags = flags + c0;
+        for (int s = 0; s < S.patch_iters; ++s) {
+          sa.pub = s == 0 ? nullptr : (s & 1 ? d.xb : d.xa) + 6 * pG;
+          sa.next = (s & 1 ? d.xa : d.xb) + 6 * pG;
+          sa.last = s == S.patch_iters - 1;
+          launch_schwarz(sa, bc, st);
+          L.count += 1;
+        }
+      } else {
+        PcgArgs ga{};
+        ga.gw = d.gw; ga.gh = d.gh; ga.iters = S.pcg_iters; ga.sys = na.sys;
+        ga.x = sc.px + 6 * pG; ga.r = sc.pr + 6 * pG; ga.z = sc.pz + 6 * pG; ga.p = sc.pp + 6 * pG;
+        ga.ap = sc.pap + 6 * pG; ga.trace = nullptr; ga.update = 1; ga.delta = d.delta + 6 * pG;
+        ga.total = d.total + 6 * pG; ga.base = d.base + 6 * pG; ga.active = S.active_fields; ga.flags = flags + c0;
+        launch_pcg_global(ga, bc, st);
         L.count += 1;
       }
-    } else {
-      PcgArgs ga{};
-      ga.gw = d.gw; ga.gh = d.gh; ga.iters = S.pcg_iters; ga.sys = d.sys;
-      ga.x = sc.px; ga.r = sc.pr; ga.z = sc.pz; ga.p = sc.pp; ga.ap = sc.pap; ga.trace = nullptr;
-      ga.update = 1; ga.delta = d.delta; ga.total = d.total; ga.base = d.base; ga.active = S.active_fields;
-      ga.flags = flags;
-      launch_pcg_global(ga, B, st);
-      L.count += 1;
     }
+    d.nodew = wnew;
   }
-  if (gn > 0) {  // E_after of the last iteration (solver.cpp:523-528)
+  if (gn > 0) {  // E_after of the last iteration (solver.cpp:523-528), whole batch
+    PixArgs pa{};
+    pa.w = d.w; pa.h = d.h; pa.gw = d.gw; pa.gh = d.gh; pa.step = d.step; pa.ncx = d.ncx; pa.ncy = d.ncy;
+    pa.tcx = d.tcx; pa.tcy = d.tcy; pa.rp = d.rp;
+    pa.pk = d.pk; pa.gy = d.gy; pa.illum = d.illum; pa.vis4 = d.vis; pa.W = d.W; pa.total = d.total; pa.half = d.half;
+    pa.cells = d.cells; pa.ep_pair = eps; pa.flags = flags; pa.P = to_params(P); pa.active = S.active_fields;
     pa.refresh = 0;
     pa.ep_new = E.slot(slot_base + 2 * (gn - 1) + 1);
     pa.ep_old = nullptr;
     launch_pixel(false, pa, B, st);
-    na.refresh = 0;
-    na.node_w = d.nodew;
-    na.node_w_new = d.nodew;
+    NodeArgs na{};
+    na.w = d.w; na.h = d.h; na.gw = d.gw; na.gh = d.gh; na.step = d.step; na.ncx = d.ncx; na.ncy = d.ncy;
+    na.half = d.half; na.node_w = d.nodew; na.node_w_new = d.nodew; na.total = d.total; na.delta = d.delta;
+    na.cells = d.cells; na.sys = d.sys; na.ep_pair = eps; na.ep_base = d.n_pix_cta; na.flags = flags;
+    na.P = to_params(P); na.F = dF; na.active = S.active_fields; na.lm = S.lm_lambda; na.refresh = 0;
     na.ep_new = pa.ep_new;
     na.ep_old = nullptr;
     launch_node(false, na, B, st);
@@ -336,7 +363,10 @@ struct Plan {
     if (outmask & 8) o_disp = mem.alloc<double>(B * N0);
     if (profile) {
       int total_gn = 0;
-      for (int l = 0; l < L; ++l) total_gn += gn[l];
+      for (int l = 0; l < L; ++l) {
+        const int ch = level_chunk(lv[l], B, l);
+        total_gn += gn[l] * ((B + ch - 1) / ch);
+      }
       ev.resize(2 * std::max(total_gn, 1));
       for (auto& e : ev) CK(cudaEventCreate(&e));
     }
@@ -393,7 +423,7 @@ struct Plan {
       }
       CK(cudaMemsetAsync(d.W, 1, B * d.N, st));
       CK(cudaMemsetAsync(d.nodew, 0, sizeof(double) * B * d.G, st));
-      record_gn_level(d, B, P, S, dF, gn[l], E, slot_base[l], sc, flags, st, LC);
+      record_gn_level(d, B, P, S, dF, gn[l], E, slot_base[l], sc, flags, st, LC, level_chunk(d, B, l));
       launch_occlusion(d.w, d.h, d.gw, d.gh, d.step, d.total, B, sc.q, sc.Z, sc.bad, sc.zbuf, sc.degen, sc.queue,
                        sc.qcount, d.occ, st);
       LC.count += 4;
