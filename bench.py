@@ -251,29 +251,43 @@ def run_ours(args, ws, rank, local):
     pairs = shard(rank, ws, B)
     frames_np = make_frames(B, pairs.start)
     host_in = torch.from_numpy(frames_np).pin_memory()
-    host_grid = torch.empty((B, G, 6), dtype=torch.float64).pin_memory()
-    host_vis = torch.empty((B, H_, W_), dtype=torch.uint8).pin_memory()
+    # two result slots (the streaming API keeps two batches in flight)
+    host_grid = [torch.empty((B, G, 6), dtype=torch.float64).pin_memory() for _ in range(2)]
+    host_vis = [torch.empty((B, H_, W_), dtype=torch.uint8).pin_memory() for _ in range(2)]
     fr = (Frame4C * B)()
-    res = (ResultC * B)()
+    res = [(ResultC * B)() for _ in range(2)]
     base = host_in.data_ptr()
     for i in range(B):
         fr[i].width, fr[i].height, fr[i].dtype = W_, H_, DTYPE_U8
         for e in range(4):
             fr[i].plane[e] = base + (4 * i + e) * N
-        res[i].grid_total = C.cast(host_grid.data_ptr() + i * G * 6 * 8, capi._dp)
-        res[i].vis4 = C.cast(host_vis.data_ptr() + i * N, capi._u8p)
-    stats = (StatsC * B)()
+        for k in range(2):
+            res[k][i].grid_total = C.cast(host_grid[k].data_ptr() + i * G * 6 * 8, capi._dp)
+            res[k][i].vis4 = C.cast(host_vis[k].data_ptr() + i * N, capi._u8p)
+    stats = [(StatsC * B)() for _ in range(2)]
 
     lib.hwf_set_profiling(h, 1)
     d_in, d_grid = C.c_void_p(), C.c_void_p()
     dev.ctx.check(lib.hwf_prepare_device(h, B, W_, H_, DTYPE_U8, C.byref(pc), C.byref(sc), dptr(None),
                                          C.byref(d_in), C.byref(d_grid)))
 
-    def e2e_step():
-        rc = lib.hwf_solve_batch(h, B, fr, C.byref(pc), C.byref(sc), dptr(None), res, stats)
+    def ok(rc):
         if rc not in (capi.HWF_OK, capi.HWF_EDIVERGED):  # divergence is the reference's own behaviour; reported
             dev.ctx.check(rc)
         return rc
+
+    def e2e_step():
+        return ok(lib.hwf_solve_batch(h, B, fr, C.byref(pc), C.byref(sc), dptr(None), res[0], stats[0]))
+
+    def e2e_stream(steps):
+        """steps batches through hwf_submit_batch/hwf_wait: every step uploads its u8 frames from
+        pinned host memory and downloads its finest grid + visibility; transfers of neighbouring
+        steps overlap the current step's device solve."""
+        for i in range(steps):
+            ok(lib.hwf_submit_batch(h, B, fr, C.byref(pc), C.byref(sc), dptr(None), res[i % 2], stats[i % 2]))
+            if i >= 1:
+                ok(lib.hwf_wait(h))
+        ok(lib.hwf_wait(h))
 
     # warm-up (also fills the plan's device input buffer with this rank's frames)
     for _ in range(args.warmup):
@@ -297,7 +311,7 @@ def run_ours(args, ws, rank, local):
     ms_total = allreduce_max(ev0.elapsed_time(ev1), ws)
     ms_per_step = ms_total / args.steps
     value = ws * B * args.steps / (ms_total / 1000.0)
-    rc_sync = lib.hwf_sync(h, stats)
+    rc_sync = lib.hwf_sync(h, stats[0])
 
     # dominant kernel (k_pixel<LIN>) timings from the last replay, CUDA events inside the graph
     cap = 64
@@ -319,9 +333,11 @@ def run_ours(args, ws, rank, local):
     # ---- e2e: through the public C-ABI from pinned host buffers ---------------------
     barrier(ws)
     torch.cuda.synchronize()
+    e2e_stream(2)  # warm the streaming slots (second graph capture)
+    torch.cuda.synchronize()
+    barrier(ws)
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        e2e_step()
+    e2e_stream(args.steps)
     t1 = time.perf_counter()
     barrier(ws)
     e2e_s = allreduce_max(t1 - t0, ws)

@@ -34,6 +34,16 @@ int hwf_launch_count(hwf_ctx* ctx);
 /* Per-launch duration (ms) and algorithmic bytes of k_pixel<LIN> from the last replay. */
 int hwf_pixel_kernel_times(hwf_ctx* ctx, int cap, double* ms, double* bytes);
 
+/* Streaming: enqueue one batch from host memory and return immediately; batch k's
+ * upload and batch k-1's download overlap batch k's device solve (two slots, at
+ * most two batches in flight). Results (grid_total, vis4 only) and stats become
+ * valid when hwf_wait returns for that batch. */
+int hwf_submit_batch(hwf_ctx* ctx, int n_pairs, const hwf_frame4* frames, const hwf_energy_params* params,
+                     const hwf_schedule* sched, const double* fundamental, hwf_result* out,
+                     hwf_stats* stats);
+/* Complete the oldest submitted batch (blocking); HWF_EDIVERGED if a pair diverged. */
+int hwf_wait(hwf_ctx* ctx);
+
 #ifdef __cplusplus
 }
 #endif

@@ -52,9 +52,11 @@ int hwf_create(int device, hwf_ctx** out) {
 void hwf_destroy(hwf_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
-  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (cudaStream_t s : {ctx->stream, ctx->h2d, ctx->d2h})
+    if (s) cudaStreamSynchronize(s);
   ctx->plan.reset();
-  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  for (cudaStream_t s : {ctx->stream, ctx->h2d, ctx->d2h})
+    if (s) cudaStreamDestroy(s);
   delete ctx;
 }
 
@@ -125,6 +127,7 @@ int hwf_solve_batch(hwf_ctx* ctx, int n, const hwf_frame4* frames, const hwf_ene
                     const hwf_schedule* sched, const double* F, hwf_result* out, hwf_stats* stats) {
   return guard(ctx, [&] {
     if (n < 1 || !frames || !out) throw InvalidArg("bad batch");
+    if (!ctx->inflight.empty()) throw InvalidArg("streaming batches in flight: call hwf_wait first");
     check_params(params, sched, F);
     const int w = frames[0].width, h = frames[0].height, dt = frames[0].dtype;
     if (w < 1 || h < 1) throw InvalidArg("bad frame dims");
@@ -256,6 +259,105 @@ int hwf_solve_batch_seq(hwf_ctx* ctx, int n, const hwf_frame4* frames, const hwf
 int hwf_solve_pair(hwf_ctx* ctx, const hwf_frame4* frames, const hwf_energy_params* params,
                    const hwf_schedule* sched, const double* F, hwf_result* out, hwf_stats* stats) {
   return hwf_solve_batch(ctx, 1, frames, params, sched, F, out, stats);
+}
+
+// ---- streaming (hwflow_ext.h): overlap batch k+1's upload and batch k-1's download
+// with batch k's graph. Two slots; at most two batches in flight.
+int hwf_submit_batch(hwf_ctx* ctx, int n, const hwf_frame4* frames, const hwf_energy_params* params,
+                     const hwf_schedule* sched, const double* F, hwf_result* out, hwf_stats* stats) {
+  return guard(ctx, [&] {
+    if (n < 1 || !frames || !out) throw InvalidArg("bad batch");
+    if (ctx->inflight.size() >= 2) throw InvalidArg("two batches in flight: call hwf_wait first");
+    check_params(params, sched, F);
+    const int w = frames[0].width, h = frames[0].height, dt = frames[0].dtype;
+    for (int i = 0; i < n; ++i) {
+      if (frames[i].width != w || frames[i].height != h || frames[i].dtype != dt)
+        throw InvalidArg("all pairs of a batch must share size and dtype");
+      if (out[i].s || out[i].m || out[i].d || out[i].disparity)
+        throw InvalidArg("streaming returns grid_total and vis4 only (dense fields: hwf_solve_batch)");
+    }
+    Plan& p = get_plan(ctx, n, w, h, dt, params, sched, F, 0u);
+    if (!ctx->h2d) {
+      CK(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
+    }
+    p.ensure_async(ctx->stream);
+    const int k = ctx->next_slot;
+    ctx->next_slot ^= 1;
+    const size_t N = p.lv[0].N, G = p.lv[0].G, esz = dt == HWF_DTYPE_U8 ? 1 : 8;
+    // upload into slot k once the slot's previous graph has consumed it
+    CK(cudaStreamWaitEvent(ctx->h2d, p.ev_comp[k], 0));
+    bool contiguous = true;
+    const char* base = static_cast<const char*>(frames[0].plane[0]);
+    for (int i = 0; i < n && contiguous; ++i)
+      for (int e = 0; e < 4; ++e)
+        contiguous = contiguous && static_cast<const char*>(frames[i].plane[e]) == base + (4 * static_cast<size_t>(i) + e) * N * esz;
+    if (contiguous) {
+      CK(cudaMemcpyAsync(p.in_slot[k], base, 4 * n * N * esz, cudaMemcpyHostToDevice, ctx->h2d));
+    } else {
+      for (int i = 0; i < n; ++i)
+        for (int e = 0; e < 4; ++e)
+          CK(cudaMemcpyAsync(static_cast<char*>(p.in_slot[k]) + (4 * static_cast<size_t>(i) + e) * N * esz,
+                             frames[i].plane[e], N * esz, cudaMemcpyHostToDevice, ctx->h2d));
+    }
+    CK(cudaEventRecord(p.ev_h2d[k], ctx->h2d));
+    // compute, then snapshot the results the next graph would overwrite
+    CK(cudaStreamWaitEvent(ctx->stream, p.ev_h2d[k], 0));
+    CK(cudaGraphLaunch(p.exec_slot[k], ctx->stream));
+    CK(cudaMemcpyAsync(p.st_grid[k], p.lv[0].total, sizeof(double) * n * G * 6, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(p.st_occ[k], p.lv[0].occ, n * N, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(p.st_red[k], p.E.red, sizeof(double) * n * p.E.nslots * kNumEnergy, cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+    CK(cudaMemcpyAsync(p.st_flags[k], p.flags, sizeof(int) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaEventRecord(p.ev_comp[k], ctx->stream));
+    // download on the second copy stream
+    CK(cudaStreamWaitEvent(ctx->d2h, p.ev_comp[k], 0));
+    for (int i = 0; i < n; ++i) {
+      if (out[i].grid_total)
+        CK(cudaMemcpyAsync(out[i].grid_total, p.st_grid[k] + i * G * 6, G * 6 * sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->d2h));
+      if (out[i].vis4) CK(cudaMemcpyAsync(out[i].vis4, p.st_occ[k] + i * N, N, cudaMemcpyDeviceToHost, ctx->d2h));
+    }
+    CK(cudaMemcpyAsync(p.h_red[k], p.st_red[k], sizeof(double) * n * p.E.nslots * kNumEnergy, cudaMemcpyDeviceToHost,
+                       ctx->d2h));
+    CK(cudaMemcpyAsync(p.h_flags[k], p.st_flags[k], sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->d2h));
+    CK(cudaEventRecord(p.ev_d2h[k], ctx->d2h));
+    hwf_inflight f;
+    f.slot = k;
+    f.n = n;
+    f.out.assign(out, out + n);
+    f.stats = stats;
+    ctx->inflight.push_back(std::move(f));
+  });
+}
+
+int hwf_wait(hwf_ctx* ctx) {
+  return guard(ctx, [&] {
+    if (ctx->inflight.empty()) throw InvalidArg("no batch in flight");
+    const hwf_inflight f = ctx->inflight.front();
+    ctx->inflight.pop_front();
+    Plan& p = *ctx->plan;
+    CK(cudaEventSynchronize(p.ev_d2h[f.slot]));
+    std::vector<int> flags(p.h_flags[f.slot], p.h_flags[f.slot] + f.n);
+    if (f.stats) {
+      const hwf_energy_params& P = p.P;
+      for (int i = 0; i < f.n; ++i) {
+        hwf_stats& s = f.stats[i];
+        std::memset(&s, 0, sizeof(s));
+        s.levels_used = p.L;
+        for (int l = 0; l < p.L; ++l) {
+          s.gn_iters[l] = p.gn[l];
+          for (int it = 0; it < p.gn[l]; ++it)
+            for (int q = 0; q < 2; ++q) {
+              const double* e = p.h_red[f.slot] + (static_cast<size_t>(i) * p.E.nslots + p.slot_base[l] + 2 * it + q) * kNumEnergy;
+              (q == 0 ? s.energy_before : s.energy_after)[l][it] =
+                  P.w_photo * e[0] + P.w_grad * e[1] + P.w_reg * (P.w_smooth * e[2] + P.w_epi * e[3] + P.w_mag * e[4]);
+            }
+        }
+      }
+    }
+    raise_on_flags(flags, f.n);
+  });
 }
 
 // ---- device-resident extensions (hwflow_ext.h) -----------------------------------

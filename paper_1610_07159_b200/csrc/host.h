@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -299,6 +300,18 @@ struct Plan {
   double *o_s = nullptr, *o_m = nullptr, *o_d = nullptr, *o_disp = nullptr;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
+  // streaming (hwf_submit_batch / hwf_wait): two input/result slots, one graph each
+  bool async_ready = false;
+  void* in_slot[2] = {};
+  cudaGraph_t graph2 = nullptr;
+  cudaGraphExec_t exec_slot[2] = {};
+  double* st_grid[2] = {};
+  uint8_t* st_occ[2] = {};
+  double* st_red[2] = {};
+  int* st_flags[2] = {};
+  double* h_red[2] = {};  // pinned
+  int* h_flags[2] = {};   // pinned
+  cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
   int launches = 0;
   std::vector<cudaEvent_t> ev;
   std::vector<double> ev_bytes;
@@ -314,7 +327,53 @@ struct Plan {
   ~Plan() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
+    if (exec_slot[1]) cudaGraphExecDestroy(exec_slot[1]);
+    if (graph2) cudaGraphDestroy(graph2);
     for (auto e : ev) cudaEventDestroy(e);
+    for (int k = 0; k < 2; ++k) {
+      if (h_red[k]) cudaFreeHost(h_red[k]);
+      if (h_flags[k]) cudaFreeHost(h_flags[k]);
+      for (cudaEvent_t e : {ev_h2d[k], ev_comp[k], ev_d2h[k]})
+        if (e) cudaEventDestroy(e);
+    }
+  }
+
+  // Second input slot + its own captured graph + result staging (streaming API).
+  void ensure_async(cudaStream_t st) {
+    if (async_ready) return;
+    const size_t N0 = lv[0].N, G0 = lv[0].G;
+    in_slot[0] = in;
+    in_slot[1] = dtype == HWF_DTYPE_U8 ? static_cast<void*>(mem.alloc<uint8_t>(B * 4 * N0))
+                                       : static_cast<void*>(mem.alloc<double>(B * 4 * N0));
+    for (int k = 0; k < 2; ++k) {
+      st_grid[k] = mem.alloc<double>(B * G0 * 6);
+      st_occ[k] = mem.alloc<uint8_t>(B * N0);
+      st_red[k] = mem.alloc<double>(static_cast<size_t>(B) * E.nslots * kNumEnergy);
+      st_flags[k] = mem.alloc<int>(B);
+      CK(cudaMallocHost(&h_red[k], sizeof(double) * B * E.nslots * kNumEnergy));
+      CK(cudaMallocHost(&h_flags[k], sizeof(int) * B));
+      CK(cudaEventCreateWithFlags(&ev_h2d[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ev_comp[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ev_d2h[k], cudaEventDisableTiming));
+    }
+    // capture the same pipeline reading slot 1 (w_i ping-pong restarts from buffer a)
+    for (int l = 0; l < L; ++l) lv[l].nodew = lv[l].nodew_a;
+    in = in_slot[1];
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    try {
+      record(st);
+    } catch (...) {
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(st, &g);
+      if (g) cudaGraphDestroy(g);
+      in = in_slot[0];
+      throw;
+    }
+    CK(cudaStreamEndCapture(st, &graph2));
+    CK(cudaGraphInstantiate(&exec_slot[1], graph2, 0));
+    exec_slot[0] = exec;
+    in = in_slot[0];
+    async_ready = true;
   }
 
   void build(cudaStream_t st) {
@@ -461,12 +520,21 @@ struct hwf_state {
   }
 };
 
+struct hwf_inflight {  // one submitted streaming batch
+  int slot = 0, n = 0;
+  std::vector<hwf_result> out;
+  hwf_stats* stats = nullptr;
+};
+
 struct hwf_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of the streaming API
   std::string err;
   std::unique_ptr<hwf_host::Plan> plan;
   bool profile = false;
+  std::deque<hwf_inflight> inflight;
+  int next_slot = 0;
 };
 
 namespace hwf_host {
@@ -525,6 +593,7 @@ inline void upload_frames(Plan& p, int n, const hwf_frame4* fr, cudaStream_t st)
 inline Plan& get_plan(hwf_ctx* ctx, int n, int w, int h, int dtype, const hwf_energy_params* P, const hwf_schedule* S,
                const double* F, unsigned outmask, bool has_prev = false) {
   if (ctx->plan && ctx->plan->matches(n, w, h, dtype, *P, *S, F, outmask, ctx->profile, has_prev)) return *ctx->plan;
+  if (!ctx->inflight.empty()) throw InvalidArg("a different configuration was requested while batches are in flight");
   ctx->plan.reset();
   CK(cudaStreamSynchronize(ctx->stream));
   auto p = std::make_unique<Plan>();

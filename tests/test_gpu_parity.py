@@ -320,3 +320,42 @@ def test_sequence_matches_oracle(device, oracle):
             db, tb = oprev[i].read(0)
             for l in range(len(da)):
                 assert np.abs(ta[l] - tb[l]).max() < FLOW_TOL_PX
+
+
+def test_streaming_submit_wait_matches_sync(device):
+    """hwf_submit_batch/hwf_wait (two batches in flight, transfers overlapping compute) return
+    exactly what hwf_solve_batch returns."""
+    import ctypes as C
+    from paper_1610_07159_b200 import capi
+    frames = [np.stack([synthetic.webcam_pair(4 * k + i, 128, 96)[0] for i in range(4)]) for k in range(3)]
+    S = SolveSchedule(levels=3, grid_step=8, pcg_iters=5, patch_iters=5)
+    P = EnergyParams()
+    ref = [device.solve_batch(f, P, S, outputs=("grid_total", "vis4")) for f in frames]
+    lib, h = device.lib, device.ctx.h
+    gw, gh = grid_dims(128, 96, 8)
+    keep, outs = [], []
+    pc, sc = P.to_c(), S.to_c()
+    for k, f in enumerate(frames):
+        fr = (capi.Frame4C * 4)()
+        res = (capi.ResultC * 4)()
+        st = (capi.StatsC * 4)()
+        grids = np.empty((4, gw * gh, 6))
+        vis = np.empty((4, 96, 128), np.uint8)
+        for i in range(4):
+            fr[i].width, fr[i].height, fr[i].dtype = 128, 96, capi.DTYPE_U8
+            for e in range(4):
+                fr[i].plane[e] = f[i, e].ctypes.data
+            res[i].grid_total = capi.dptr(grids[i])
+            res[i].vis4 = capi.u8ptr(vis[i])
+        keep.append((fr, res, st, grids, vis, f))
+        device.ctx.check(lib.hwf_submit_batch(h, 4, fr, C.byref(pc), C.byref(sc), capi.dptr(None), res, st))
+        if k >= 1:
+            device.ctx.check(lib.hwf_wait(h))
+    device.ctx.check(lib.hwf_wait(h))
+    for k in range(3):
+        (_, _, st, grids, vis, _) = keep[k]
+        outs_ref, stats_ref = ref[k]
+        for i in range(4):
+            assert np.array_equal(grids[i], outs_ref[i].grid_total)
+            assert np.array_equal(vis[i], outs_ref[i].vis4)
+            assert st[i].energy_after[0][1] == stats_ref[i].energy_after[0][1]
