@@ -34,6 +34,7 @@ struct PixArgs {
   Params P;
   uint32_t active;
   int refresh;
+  double* resid;        // optional stacked R (energy.cpp:208-228): photo [0,N), grad [N,2N)
 };
 
 struct NodeArgs {
@@ -55,6 +56,8 @@ struct NodeArgs {
   uint32_t active;
   double lm;
   int refresh;
+  double* resid;        // optional stacked R: smooth [2N,2N+6G), epi [..+2G), mag [..+6G)
+  long long resid_n;    // N of the level (offset of the node blocks)
 };
 
 struct SwzArgs {

@@ -197,19 +197,22 @@ int hwf_eval_energy(hwf_ctx* ctx, const hwf_level* lv, const hwf_energy_params* 
     if (!P || !out) throw InvalidArg("null argument");
     if (hwf_validate_params(P) != HWF_OK) throw InvalidArg("energy weights must be >= 0");
     if (P->w_epi > 0.0 && !lv->fundamental) throw InvalidArg("epipolar term enabled without a fundamental matrix");
-    if (residuals) throw InvalidArg("residual vector output is not provided by the device library");
     DevMem m;
     LevelDev d;
     load_level(m, d, lv, false, 0, ctx->stream);
+    double* dR = residuals ? m.alloc<double>(2 * d.N + 14 * d.G) : nullptr;
     const double* dF = lv->fundamental ? up(m, lv->fundamental, 9) : nullptr;
     Energies E;
     make_energies(m, E, d, 1);
     int* flags = up<int>(m, nullptr, 1);
     PixArgs pa = pix_args(d, P, 7u, flags, E);
     pa.refresh = 0;
+    pa.resid = dR;
     launch_pixel(false, pa, 1, ctx->stream);
     NodeArgs na = node_args(d, P, 7u, 0.0, dF, flags, E);
     na.refresh = 0;
+    na.resid = dR;
+    na.resid_n = static_cast<long long>(d.N);
     launch_node(false, na, 1, ctx->stream);
     launch_energy_reduce(E.part, E.nslots, E.cap, 1, E.red, flags, ctx->stream);
     CK(cudaStreamSynchronize(ctx->stream));
@@ -223,6 +226,7 @@ int hwf_eval_energy(hwf_ctx* ctx, const hwf_level* lv, const hwf_energy_params* 
     out->mag = e[4];
     out->total = P->w_photo * e[0] + P->w_grad * e[1] + P->w_reg * (P->w_smooth * e[2] + P->w_epi * e[3] + P->w_mag * e[4]);
     out->residual_count = 2LL * static_cast<long long>(d.N) + 14LL * static_cast<long long>(d.G);
+    if (residuals) down(residuals, dR, static_cast<size_t>(out->residual_count));
     if (!std::isfinite(out->total)) throw Diverged("non-finite residuals in energy assembly");
   });
 }

@@ -359,3 +359,42 @@ def test_streaming_submit_wait_matches_sync(device):
             assert np.array_equal(grids[i], outs_ref[i].grid_total)
             assert np.array_equal(vis[i], outs_ref[i].vis4)
             assert st[i].energy_after[0][1] == stats_ref[i].energy_after[0][1]
+
+
+def test_residual_vector_matches_oracle(device, oracle, golden):
+    """assemble_residuals (energy.cpp:208-228): the stacked R, M = 2N + 14G entries."""
+    for P in (EnergyParams(), EnergyParams.preset("facial")):
+        lv = _golden_level(golden)
+        ea, Ra = device.energy(lv, P, residuals=True)
+        eb, Rb = oracle.energy(lv, P, residuals=True)
+        assert Ra.size == Rb.size == ea.residual_count
+        np.testing.assert_allclose(Ra, Rb, rtol=1e-9, atol=1e-13)
+        assert (Ra ** 2).sum() == pytest.approx(ea.total, rel=1e-9)  # |R|^2 = E (SPEC acceptance 2)
+
+
+def _fd_jacobian_check(solver, lv, P, picks, h=1e-7):
+    """rhs = -J^T r must equal -(1/2) dE/dx by central differences of E(total, delta) with
+    W, V and w_i frozen (SPEC acceptance 1 through the blocked assembly)."""
+    _, rhs, _ = solver.build_normal_system(lv, P, 7, 0.0)
+    errs = []
+    for (k, c) in picks:
+        e = []
+        for sgn in (1.0, -1.0):
+            t, d = lv.total.copy(), lv.delta.copy()
+            t[k, c] += sgn * h
+            d[k, c] += sgn * h
+            lv2 = LevelState(lv.images, lv.grid_step, t, d, lv.vis4, lv.outlier, lv.node_w, lv.illum, lv.fundamental)
+            e.append(solver.energy(lv2, P)[0].total)
+        fd = -(e[0] - e[1]) / (2 * h) / 2.0
+        errs.append(abs(fd - rhs[6 * k + c]) / max(abs(rhs[6 * k + c]), 1e-3 * np.abs(rhs).max()))
+    return np.array(errs)
+
+
+def test_jacobian_finite_differences(device, oracle):
+    rng = np.random.default_rng(11)
+    lv = _random_level(31, 40, 32, 4)
+    G = lv.total.shape[0]
+    picks = [(int(rng.integers(G)), int(rng.integers(6))) for _ in range(24)]
+    for s in (device, oracle):
+        errs = _fd_jacobian_check(s, lv, EnergyParams.preset("facial"), picks)
+        assert np.median(errs) < 1e-5 and (errs < 1e-3).mean() >= 0.9, errs

@@ -249,3 +249,18 @@ def test_sequence_propagation_lowers_initial_energy(oracle):
         prev = st[k % 2]
     (_,), (cold,) = oracle.solve_batch(pairs[2][None], P, S)
     assert s.energy_before[0][0] < cold.energy_before[0][0]
+
+
+def test_jacobian_finite_differences_oracle():
+    """CPU-only variant of the SPEC acceptance-1 check on the oracle (the GPU test repeats it on the device)."""
+    import importlib
+    from paper_1610_07159_b200 import build
+    from paper_1610_07159_b200.hwflow import Solver
+    gp = importlib.import_module("test_gpu_parity")
+    orc = Solver(build.ORACLE_LIB)
+    rng = np.random.default_rng(11)
+    lv = gp._random_level(31, 40, 32, 4)
+    G = lv.total.shape[0]
+    picks = [(int(rng.integers(G)), int(rng.integers(6))) for _ in range(24)]
+    errs = gp._fd_jacobian_check(orc, lv, EnergyParams.preset("facial"), picks)
+    assert np.median(errs) < 1e-5 and (errs < 1e-3).mean() >= 0.9, errs
