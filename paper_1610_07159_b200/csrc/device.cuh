@@ -162,6 +162,7 @@ __device__ __forceinline__ void sample_img(const double* __restrict__ I, int w, 
 // corner offsets, the in-cell fractions and whether each coordinate is clamped.
 struct Foot {
   int o00, o10, o01, o11;
+  int x0, y0;  // the (x, y) of o00
   double fx, fy;
   bool clx, cly;
 };
@@ -173,6 +174,8 @@ __device__ __forceinline__ Foot footprint(int w, int h, double x, double y) {
   f.o10 = cy.i0 * w + c2;
   f.o01 = r2 * w + cx.i0;
   f.o11 = r2 * w + c2;
+  f.x0 = cx.i0;
+  f.y0 = cy.i0;
   f.fx = cx.f;
   f.fy = cy.f;
   f.clx = cx.clamped;

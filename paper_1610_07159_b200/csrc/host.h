@@ -170,9 +170,10 @@ struct Launches {
 
 // Algorithmic bytes of one k_pixel<LIN> launch: every
 // input read once, every output written once.
-inline double pixel_bytes(const LevelDev& d, int B, bool illum) {
-  // {v, gx} + gy samples of 4 images, illumination, vis4 + W in/out, halfway out
-  const double perpix = 4 * 24.0 + (illum ? 4 * 8.0 : 0.0) + 1 + 1 + 1 + 8;
+inline double pixel_bytes(const LevelDev& d, int B, bool illum, bool u8) {
+  // 4 images ({v, gx} + gy sample planes, or the u8 frames at the finest level),
+  // illumination, vis4 + W in/out, halfway out
+  const double perpix = 4 * (u8 ? 1.0 : 24.0) + (illum ? 4 * 8.0 : 0.0) + 1 + 1 + 1 + 8;
   return B * (d.N * perpix + d.G * 48.0 + d.C * kCellStride * 8.0);
 }
 
@@ -196,7 +197,7 @@ inline int level_chunk(const LevelDev& d, int B, int level) {
 // The nonlinear loop of one level (solver.cpp:484-532) for a batch.
 inline void record_gn_level(LevelDev& d, int B, const hwf_energy_params& P, const hwf_schedule& S, const double* dF,
                      int gn, const Energies& E, int slot_base, Scratch& sc, int* flags, cudaStream_t st,
-                     Launches& L, int chunk = 0) {
+                     Launches& L, int chunk = 0, const uint8_t* src8 = nullptr) {
   const int CH = chunk > 0 ? std::min(chunk, B) : B;
   const long long eps = E.pair_stride();
   for (int it = 0; it < gn; ++it) {
@@ -207,7 +208,7 @@ inline void record_gn_level(LevelDev& d, int B, const hwf_energy_params& P, cons
       PixArgs pa{};
       pa.w = d.w; pa.h = d.h; pa.gw = d.gw; pa.gh = d.gh; pa.step = d.step; pa.ncx = d.ncx; pa.ncy = d.ncy;
       pa.tcx = d.tcx; pa.tcy = d.tcy; pa.rp = d.rp;
-      pa.pk = d.pk + 4 * pN; pa.gy = d.gy + 4 * pN; pa.illum = d.illum ? d.illum + 4 * pN : nullptr;
+      pa.pk = d.pk + 4 * pN; pa.gy = d.gy + 4 * pN; pa.src8 = src8 ? src8 + 4 * pN : nullptr; pa.illum = d.illum ? d.illum + 4 * pN : nullptr;
       pa.vis4 = d.vis + pN; pa.W = d.W + pN; pa.total = d.total + 6 * pG; pa.half = d.half + pN;
       pa.cells = d.cells + static_cast<size_t>(c0) * d.C * kCellStride; pa.ep_pair = eps; pa.flags = flags + c0;
       pa.P = to_params(P); pa.active = S.active_fields; pa.refresh = 1;
@@ -217,7 +218,7 @@ inline void record_gn_level(LevelDev& d, int B, const hwf_energy_params& P, cons
       launch_pixel(true, pa, bc, st);
       if (L.ev) {
         CK(cudaEventRecordWithFlags((*L.ev)[2 * L.bytes->size() + 1], st, cudaEventRecordExternal));
-        L.bytes->push_back(pixel_bytes(d, bc, d.illum != nullptr));
+        L.bytes->push_back(pixel_bytes(d, bc, d.illum != nullptr, src8 != nullptr));
       }
       launch_structw(d.w, d.h, d.gw, d.gh, d.step, d.half + pN, wnew + pG, bc, st);
       NodeArgs na{};
@@ -256,7 +257,7 @@ inline void record_gn_level(LevelDev& d, int B, const hwf_energy_params& P, cons
     PixArgs pa{};
     pa.w = d.w; pa.h = d.h; pa.gw = d.gw; pa.gh = d.gh; pa.step = d.step; pa.ncx = d.ncx; pa.ncy = d.ncy;
     pa.tcx = d.tcx; pa.tcy = d.tcy; pa.rp = d.rp;
-    pa.pk = d.pk; pa.gy = d.gy; pa.illum = d.illum; pa.vis4 = d.vis; pa.W = d.W; pa.total = d.total; pa.half = d.half;
+    pa.pk = d.pk; pa.gy = d.gy; pa.src8 = src8; pa.illum = d.illum; pa.vis4 = d.vis; pa.W = d.W; pa.total = d.total; pa.half = d.half;
     pa.cells = d.cells; pa.ep_pair = eps; pa.flags = flags; pa.P = to_params(P); pa.active = S.active_fields;
     pa.refresh = 0;
     pa.ep_new = E.slot(slot_base + 2 * (gn - 1) + 1);
@@ -338,13 +339,20 @@ struct Plan {
     }
   }
 
+  // The finest level of u8 frames samples the frames themselves (k_pixel<*, U8>).
+  bool u8_finest(int l) const { return l == 0 && dtype == HWF_DTYPE_U8; }
+  // Device input frames; u8 frames get 16 B of padding on both sides (ld4u8).
+  void* alloc_input(size_t N0) {
+    if (dtype == HWF_DTYPE_U8) return mem.alloc<uint8_t>(B * 4 * N0 + 32) + 16;
+    return mem.alloc<double>(B * 4 * N0);
+  }
+
   // Second input slot + its own captured graph + result staging (streaming API).
   void ensure_async(cudaStream_t st) {
     if (async_ready) return;
     const size_t N0 = lv[0].N, G0 = lv[0].G;
     in_slot[0] = in;
-    in_slot[1] = dtype == HWF_DTYPE_U8 ? static_cast<void*>(mem.alloc<uint8_t>(B * 4 * N0))
-                                       : static_cast<void*>(mem.alloc<double>(B * 4 * N0));
+    in_slot[1] = alloc_input(N0);
     for (int k = 0; k < 2; ++k) {
       st_grid[k] = mem.alloc<double>(B * G0 * 6);
       st_occ[k] = mem.alloc<uint8_t>(B * N0);
@@ -390,13 +398,14 @@ struct Plan {
       cap = std::max(cap, static_cast<size_t>(lv[l].n_pix_cta + lv[l].n_node_cta));
     }
     const size_t N0 = lv[0].N;
-    in = dtype == HWF_DTYPE_U8 ? static_cast<void*>(mem.alloc<uint8_t>(B * 4 * N0))
-                               : static_cast<void*>(mem.alloc<double>(B * 4 * N0));
+    in = alloc_input(N0);
     for (int l = 0; l < L; ++l) {
       LevelDev& d = lv[l];
       d.img = mem.alloc<double>(B * 4 * d.N);
-      d.pk = mem.alloc<double2>(B * 4 * d.N);
-      d.gy = mem.alloc<double>(B * 4 * d.N);
+      if (!u8_finest(l)) {
+        d.pk = mem.alloc<double2>(B * 4 * d.N);
+        d.gy = mem.alloc<double>(B * 4 * d.N);
+      }
       d.alloc_solver(mem, B, S.subdomain_px > 0);
       d.occ = mem.alloc<uint8_t>(B * d.N);
       if (l < L - 1) d.illum = mem.alloc<double>(B * 4 * d.N);
@@ -460,6 +469,7 @@ struct Plan {
       LC.count++;
     }
     for (int l = 0; l < L; ++l) {
+      if (u8_finest(l)) continue;
       launch_pack(lv[l].img, lv[l].w, lv[l].h, 4 * B, lv[l].pk, lv[l].gy, st);
       LC.count++;
     }
@@ -482,7 +492,8 @@ struct Plan {
       }
       CK(cudaMemsetAsync(d.W, 1, B * d.N, st));
       CK(cudaMemsetAsync(d.nodew, 0, sizeof(double) * B * d.G, st));
-      record_gn_level(d, B, P, S, dF, gn[l], E, slot_base[l], sc, flags, st, LC, level_chunk(d, B, l));
+      record_gn_level(d, B, P, S, dF, gn[l], E, slot_base[l], sc, flags, st, LC, level_chunk(d, B, l),
+                      u8_finest(l) ? static_cast<const uint8_t*>(in) : nullptr);
       launch_occlusion(d.w, d.h, d.gw, d.gh, d.step, d.total, B, sc.q, sc.Z, sc.bad, sc.zbuf, sc.degen, sc.queue,
                        sc.qcount, d.occ, st);
       LC.count += 4;

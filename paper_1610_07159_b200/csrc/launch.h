@@ -21,6 +21,7 @@ struct PixArgs {
   int w, h, gw, gh, step, ncx, ncy, tcx, tcy, rp;
   const double2* pk;    // [B][4][N] {value, grad x} (k_pack)
   const double* gy;     // [B][4][N] grad y (k_pack)
+  const uint8_t* src8;  // [B][4][N] u8 frames of the finest level (then pk/gy unused), or null
   const double* illum;  // [B][4][N] or null
   const uint8_t* vis4;  // [B][N]
   uint8_t* W;           // [B][N] in: current bits; out: refreshed bits (refresh)

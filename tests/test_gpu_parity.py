@@ -242,6 +242,25 @@ def test_batch_is_bitwise_independent(device):
     assert all(np.array_equal(a.grid_total, b.grid_total) for a, b in zip(batch, again))
 
 
+@pytest.mark.parametrize("w,h", [(128, 96), (131, 97)])
+def test_u8_finest_level_matches_f64_frames_bitwise(device, w, h):
+    """The finest level of u8 frames is sampled from the bytes (k/255 rebuilt in registers); it must be
+    bitwise identical to the packed-plane path that f64 frames k/255 take (k_pyr_in, k_pack)."""
+    frames = np.stack([synthetic.webcam_pair(i, w, h)[0] for i in range(2)])
+    frames[0, 2, :, :7] = 255  # saturated border columns
+    frames[1, 1, -3:, :] = 0
+    f64 = frames.astype(np.float64) / 255.0
+    for S in (SolveSchedule(levels=3, grid_step=8, pcg_iters=5, patch_iters=5),
+              SolveSchedule(levels=2, grid_step=4, gn_per_level=[3, 2], pcg_iters=6, subdomain_px=0,
+                            coarse_s_offset=(2.5, -1.0))):
+        a, sa = device.solve_batch(frames, EnergyParams(), S)
+        b, sb = device.solve_batch(f64, EnergyParams(), S)
+        for x, y, u, v in zip(a, b, sa, sb):
+            assert np.array_equal(x.grid_total, y.grid_total)
+            assert np.array_equal(x.vis4, y.vis4)
+            assert u.energy_after == v.energy_after
+
+
 def test_cfg2_full_size_properties(device):
     """BASELINE cfg2 shape on a batch: finite, deterministic, identity scene stationary."""
     frames = np.stack([synthetic.webcam_pair(i)[0] for i in range(4)])

@@ -40,4 +40,4 @@ for _ in range(a.runs):
     dev.ctx.check(lib.hwf_run_device(h))
 lib.hwf_sync(h, None)
 dt = time.perf_counter() - t
-print(f"launches_per_replay={lib.hwf_launch_count(h)} batch={a.batch} ms_per_replay={1000 * dt / a.runs:.2f}")
+print(f"launches_per_replay={lib.hwf_launch_count(h)} batch={a.batch} ms_per_replay={1000 * dt / max(a.runs, 1):.2f}")
