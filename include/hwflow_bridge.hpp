@@ -7,6 +7,8 @@
 //   hwflow::b200::gauss_newton(...)   replaces hwflow::gauss_newton   (solver.hpp:152-154)
 //   hwflow::b200::run_scene_flow(...) is run_scene_flow
 //   hwflow::b200::build_pyramid(...)  replaces hwflow::build_pyramid  (image.hpp:83)
+//   hwflow::b200::{validate, triangulate_dlt, compute_scene_points, export_mesh_obj}
+//                                      are the geometry.hpp:20-59 declarations
 // Same argument meaning; SolverDivergence / std::invalid_argument are thrown
 // where the reference throws them (core.hpp:19, energy.cpp:40-50).
 #pragma once
@@ -182,6 +184,83 @@ inline FlowResult run_scene_flow(const Device& dev, const std::array<Image, 4>& 
     finest_stats->energy_after.assign(st.energy_after[0], st.energy_after[0] + st.gn_iters[0]);
   }
   return r;
+}
+
+// ---- geometry (geometry.hpp:14-59; the reference declares these, geometry.cpp is not shipped) ----
+inline hwf_rig rig_to_c(const StereoRig& rig) {
+  hwf_rig c{};
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) c.F[3 * i + j] = rig.F(i, j);
+  c.has_projections = rig.has_projections() ? 1 : 0;
+  if (rig.has_projections())
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 4; ++j) {
+        c.P0[4 * i + j] = (*rig.P0)(i, j);
+        c.P1[4 * i + j] = (*rig.P1)(i, j);
+      }
+  return c;
+}
+
+// StereoRig::validate (geometry.hpp:20-22): throws std::invalid_argument.
+inline void validate(const Device& dev, const StereoRig& rig) {
+  const hwf_rig c = rig_to_c(rig);
+  check(dev.get(), hwf_validate_rig(dev.get(), &c));
+}
+
+// triangulate_dlt (geometry.hpp:45-48).
+inline Triangulation triangulate_dlt(const Device& dev, const Mat34& P0, const Mat34& P1, const Vec2& x0,
+                                     const Vec2& x1) {
+  double p0[12], p1[12], a[2] = {x0.x(), x0.y()}, b[2] = {x1.x(), x1.y()}, X[3];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 4; ++j) {
+      p0[4 * i + j] = P0(i, j);
+      p1[4 * i + j] = P1(i, j);
+    }
+  uint8_t ok = 0;
+  check(dev.get(), hwf_triangulate(dev.get(), 1, p0, p1, a, b, X, &ok));
+  Triangulation t;
+  t.point = Vec3(X[0], X[1], X[2]);
+  t.valid = ok != 0;
+  return t;
+}
+
+// compute_scene_points (geometry.hpp:54): fills points0/points1/scene_flow/point_valid.
+inline void compute_scene_points(const Device& dev, FlowResult& r, const StereoRig& rig) {
+  const size_t N = static_cast<size_t>(r.width) * r.height;
+  std::vector<double> s(2 * N), m(2 * N), d(2 * N), p0(3 * N), p1(3 * N), sf(3 * N);
+  for (size_t i = 0; i < N; ++i)
+    for (int k = 0; k < 2; ++k) {
+      s[2 * i + k] = r.s[i](k);
+      m[2 * i + k] = r.m[i](k);
+      d[2 * i + k] = r.d[i](k);
+    }
+  r.point_valid.assign(N, 0);
+  const hwf_rig c = rig_to_c(rig);
+  check(dev.get(), hwf_scene_points(dev.get(), r.width, r.height, s.data(), m.data(), d.data(), &c, p0.data(),
+                                    p1.data(), sf.data(), r.point_valid.data()));
+  r.points0.resize(N);
+  r.points1.resize(N);
+  r.scene_flow.resize(N);
+  for (size_t i = 0; i < N; ++i) {
+    r.points0[i] = Vec3(p0[3 * i], p0[3 * i + 1], p0[3 * i + 2]);
+    r.points1[i] = Vec3(p1[3 * i], p1[3 * i + 1], p1[3 * i + 2]);
+    r.scene_flow[i] = Vec3(sf[3 * i], sf[3 * i + 1], sf[3 * i + 2]);
+  }
+  r.has_points = true;
+}
+
+// export_mesh_obj (geometry.hpp:56-59).
+inline void export_mesh_obj(const Device& dev, const FlowResult& r, const std::string& path) {
+  const size_t N = static_cast<size_t>(r.width) * r.height;
+  std::vector<double> p0;
+  if (r.has_points) {
+    p0.resize(3 * N);
+    for (size_t i = 0; i < N; ++i)
+      for (int k = 0; k < 3; ++k) p0[3 * i + k] = r.points0[i](k);
+  }
+  check(dev.get(), hwf_export_mesh_obj(dev.get(), r.width, r.height, r.disparity.data(), r.vis4.data(),
+                                       r.has_points ? p0.data() : nullptr,
+                                       r.has_points ? r.point_valid.data() : nullptr, path.c_str()));
 }
 
 }  // namespace hwflow::b200

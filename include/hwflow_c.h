@@ -23,6 +23,10 @@
  *   hwf_illumination   -> compute_illumination_maps SPEC.md:423-431 (no code shipped)
  *   hwf_prolongate     -> prolongate              SPEC.md:405-413 (no code shipped)
  *   hwf_propagate_temporal / hwf_solve_batch_seq -> propagate_temporal SPEC.md:432-440 (no code shipped)
+ *   hwf_validate_rig   -> StereoRig::validate     include/hwflow/geometry.hpp:20-22 (no code shipped)
+ *   hwf_triangulate    -> triangulate_dlt         include/hwflow/geometry.hpp:45-48 (no code shipped)
+ *   hwf_scene_points   -> compute_scene_points    include/hwflow/geometry.hpp:50-54 (no code shipped)
+ *   hwf_export_mesh_obj-> export_mesh_obj         include/hwflow/geometry.hpp:56-59 (no code shipped)
  *
  * Error convention (replaces the exceptions of the reference):
  *   HWF_OK 0, HWF_EINVAL 1 (std::invalid_argument / std::out_of_range),
@@ -217,6 +221,33 @@ int hwf_prolongate(hwf_ctx* ctx, int wc, int hc, int wf, int hf, int grid_step,
                    const double* total_coarse, const uint8_t* vis4_coarse,
                    const double* half_maps_coarse, double* base_fine, uint8_t* vis4_fine,
                    double* half_maps_fine);
+
+/* ---- geometry (include/hwflow/geometry.hpp, geometry.cpp not shipped) ---- */
+/* StereoRig (geometry.hpp:14-23): F with x_0^T F x_1 = 0 for x_c in camera c (the epipolar
+ * residual l^T F r of energy.cpp:176-178), and optional row-major 3x4 projections P0, P1. */
+typedef struct {
+  double F[9];
+  int has_projections;
+  double P0[12];
+  double P1[12];
+} hwf_rig;
+/* StereoRig::validate (geometry.hpp:20-22): rank(F) = 2 and, with projections, F consistent
+ * with P0, P1 on projected test points. HWF_EINVAL (message in hwf_last_error) on failure. */
+int hwf_validate_rig(hwf_ctx* ctx, const hwf_rig* rig);
+/* triangulate_dlt (geometry.hpp:45-48) for n correspondences: x0, x1 [n][2] -> X [n][3] and
+ * valid [n] (near-parallel rays flagged invalid, X = 0). */
+int hwf_triangulate(hwf_ctx* ctx, int n, const double P0[12], const double P1[12], const double* x0,
+                    const double* x1, double* X, uint8_t* valid);
+/* compute_scene_points (geometry.hpp:50-54): dense per-pixel s, m, d (2N each, pixel-major, as in
+ * hwf_result) -> points0, points1, scene_flow (3N each, nullable) and point_valid (N, nullable):
+ * triangulate_pixel (geometry.hpp:50-52) at t = 0 and t = 1. Needs rig->has_projections. */
+int hwf_scene_points(hwf_ctx* ctx, int width, int height, const double* s, const double* m,
+                     const double* d, const hwf_rig* rig, double* points0, double* points1,
+                     double* scene_flow, uint8_t* point_valid);
+/* export_mesh_obj (geometry.hpp:56-59): OBJ over the pixel grid; vertices are points0 when given
+ * (points0 and point_valid non-null), else (x, y, disparity). Serial host I/O. */
+int hwf_export_mesh_obj(hwf_ctx* ctx, int width, int height, const double* disparity, const uint8_t* vis4,
+                        const double* points0, const uint8_t* point_valid, const char* path);
 
 #ifdef __cplusplus
 }

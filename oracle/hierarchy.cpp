@@ -34,12 +34,8 @@
 #include <string>
 
 #include "backend.hpp"
+#include "ctx.hpp"
 #include "hwflow_c.h"
-
-struct hwf_ctx {
-  int threads = 1;
-  std::string err;
-};
 
 // Per-pair delta hierarchy + accumulated grids (SPEC.md:396 `prev`).
 struct hwf_state {

@@ -6,7 +6,7 @@ binding (capi.py), the reference-interface mirror (hwflow.py) and the
 synthetic stereo-sequence generator used by the bench and tests.
 """
 from .hwflow import (CUDA_LIB_PATH, EnergyParams, FlowResult, GnStats, LevelState, SolveSchedule, Solver,
-                     SolverDivergence, grid_dims, image_index)
+                     SolverDivergence, StereoRig, grid_dims, image_index)
 
 __all__ = ["CUDA_LIB_PATH", "EnergyParams", "FlowResult", "GnStats", "LevelState", "SolveSchedule", "Solver",
-           "SolverDivergence", "grid_dims", "image_index"]
+           "SolverDivergence", "StereoRig", "grid_dims", "image_index"]

@@ -59,6 +59,11 @@ class EnergyC(C.Structure):
                 ("mag", C.c_double), ("total", C.c_double), ("residual_count", C.c_int64)]
 
 
+class RigC(C.Structure):  # geometry.hpp:14-23 StereoRig
+    _fields_ = [("F", C.c_double * 9), ("has_projections", C.c_int), ("P0", C.c_double * 12),
+                ("P1", C.c_double * 12)]
+
+
 class HwflowError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(f"[{code}] {msg}")
@@ -123,6 +128,11 @@ _SIGS = {
     "hwf_illumination": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, _dp * 4, _dp, _u8p, _dp]),
     "hwf_prolongate": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _dp, _u8p, _dp, _dp,
                                  _u8p, _dp]),
+    "hwf_validate_rig": (C.c_int, [C.c_void_p, C.POINTER(RigC)]),
+    "hwf_triangulate": (C.c_int, [C.c_void_p, C.c_int, _dp, _dp, _dp, _dp, _dp, _u8p]),
+    "hwf_scene_points": (C.c_int, [C.c_void_p, C.c_int, C.c_int, _dp, _dp, _dp, C.POINTER(RigC), _dp, _dp, _dp,
+                                   _u8p]),
+    "hwf_export_mesh_obj": (C.c_int, [C.c_void_p, C.c_int, C.c_int, _dp, _u8p, _dp, _u8p, C.c_char_p]),
 }
 
 _EXT_SIGS = {

@@ -6,7 +6,8 @@ Names, argument meaning and error behaviour follow the reference
 (geometry.hpp:26-37), run_scene_flow (SPEC.md:396), gauss_newton
 (solver.hpp:152), build_pyramid (image.hpp:83), build_normal_system
 (solver.hpp:91), pcg_solve (solver.hpp:117), schwarz_iterate (solver.hpp:138),
-compute_occlusion_maps / compute_illumination_maps / prolongate (SPEC.md:405-431).
+compute_occlusion_maps / compute_illumination_maps / prolongate (SPEC.md:405-431),
+StereoRig / triangulate_dlt / compute_scene_points / export_mesh_obj (geometry.hpp:14-59).
 SolverDivergence is raised where the reference throws it (core.hpp:19).
 
 `Solver()` binds the product library (lib/libhwflow_cuda.so, sm_100a) and
@@ -21,13 +22,13 @@ from pathlib import Path
 import numpy as np
 
 from . import capi
-from .capi import (DTYPE_F64, DTYPE_U8, EnergyC, EnergyParamsC, Frame4C, LevelC, ResultC, ScheduleC, StatsC,
-                   SolverDivergence, dptr, u8ptr)
+from .capi import (DTYPE_F64, DTYPE_U8, EnergyC, EnergyParamsC, Frame4C, LevelC, ResultC, RigC, ScheduleC,
+                   StatsC, SolverDivergence, dptr, u8ptr)
 
 CUDA_LIB_PATH = Path(__file__).resolve().parent / "lib" / "libhwflow_cuda.so"
 
 __all__ = ["EnergyParams", "SolveSchedule", "FlowResult", "GnStats", "LevelState", "Solver", "SolverDivergence",
-           "image_index", "grid_dims", "level_dims", "CUDA_LIB_PATH"]
+           "StereoRig", "image_index", "grid_dims", "level_dims", "CUDA_LIB_PATH"]
 
 
 def image_index(cam: int, time: int) -> int:  # core.hpp:27
@@ -129,7 +130,7 @@ class GnStats:  # solver.hpp:142-147, one entry per level (0 = finest)
 
 
 @dataclass
-class FlowResult:  # geometry.hpp:26-37 (3D points are out of scope)
+class FlowResult:  # geometry.hpp:26-37
     width: int
     height: int
     s: np.ndarray | None = None          # (h, w, 2)
@@ -138,6 +139,44 @@ class FlowResult:  # geometry.hpp:26-37 (3D points are out of scope)
     disparity: np.ndarray | None = None  # (h, w) = 2 s_x
     vis4: np.ndarray | None = None       # (h, w) bit e = visible in image e
     grid_total: np.ndarray | None = None  # (G, 6) finest accumulated warp grid
+    has_points: bool = False             # filled by Solver.compute_scene_points
+    points0: np.ndarray | None = None    # (h, w, 3) triangulated at t = 0
+    points1: np.ndarray | None = None    # (h, w, 3) at t = 1
+    scene_flow: np.ndarray | None = None  # (h, w, 3) = points1 - points0
+    point_valid: np.ndarray | None = None  # (h, w) uint8
+
+    def pixel_count(self) -> int:
+        return self.width * self.height
+
+
+@dataclass
+class StereoRig:  # geometry.hpp:14-23: x_0^T F x_1 = 0 (energy.cpp:176-178), optional 3x4 projections
+    F: np.ndarray = field(default_factory=lambda: np.zeros((3, 3)))
+    P0: np.ndarray | None = None
+    P1: np.ndarray | None = None
+
+    def has_projections(self) -> bool:
+        return self.P0 is not None and self.P1 is not None
+
+    def to_c(self) -> RigC:
+        r = RigC()
+        r.F[:] = np.asarray(self.F, np.float64).ravel().tolist()
+        r.has_projections = int(self.has_projections())
+        if self.has_projections():
+            r.P0[:] = np.asarray(self.P0, np.float64).ravel().tolist()
+            r.P1[:] = np.asarray(self.P1, np.float64).ravel().tolist()
+        return r
+
+    @staticmethod
+    def load(path: str | Path) -> "StereoRig":
+        """Calibration file: 9 numbers (row-major F), optionally followed by 12 + 12 (P0, P1)."""
+        v = np.array(Path(path).read_text().split(), dtype=np.float64)
+        if v.size not in (9, 33):
+            raise ValueError(f"calibration file needs 9 or 33 numbers, got {v.size}")
+        rig = StereoRig(F=v[:9].reshape(3, 3))
+        if v.size == 33:
+            rig.P0, rig.P1 = v[9:21].reshape(3, 4), v[21:33].reshape(3, 4)
+        return rig
 
 
 @dataclass
@@ -409,6 +448,52 @@ class Solver:
         hm = np.empty((2, h, w))
         self.ctx.check(self.lib.hwf_illumination(self.ctx.h, w, h, step, arr, dptr(t), u8ptr(v), dptr(hm)))
         return hm
+
+    # ---- geometry (geometry.hpp:14-59) ------------------------------------
+    def validate_rig(self, rig: StereoRig) -> None:
+        """StereoRig::validate: raises InvalidArgument (a ValueError) on failure."""
+        rc = rig.to_c()
+        self.ctx.check(self.lib.hwf_validate_rig(self.ctx.h, C.byref(rc)))
+
+    def triangulate_dlt(self, P0: np.ndarray, P1: np.ndarray, x0: np.ndarray, x1: np.ndarray):
+        """Vectorised triangulate_dlt: x0, x1 (..., 2) -> points (..., 3), valid (...)."""
+        a0, a1 = np.ascontiguousarray(x0, np.float64), np.ascontiguousarray(x1, np.float64)
+        shape = a0.shape[:-1]
+        n = int(np.prod(shape)) if shape else 1
+        X, ok = np.zeros(shape + (3,)), np.zeros(shape, np.uint8)
+        p0, p1 = np.ascontiguousarray(P0, np.float64), np.ascontiguousarray(P1, np.float64)
+        self.ctx.check(self.lib.hwf_triangulate(self.ctx.h, n, dptr(p0), dptr(p1), dptr(a0), dptr(a1), dptr(X),
+                                                u8ptr(ok)))
+        return X, ok.astype(bool)
+
+    def triangulate_pixel(self, x, f, t: int, rig: StereoRig):
+        """geometry.hpp:50-52: f = (s, m, d) Vec2s; the correspondence (warp_position(x,f,0,t), (x,f,1,t))."""
+        x, (s, m, d) = np.asarray(x, np.float64), (np.asarray(v, np.float64) for v in f)
+        st = 1.0 if t else -1.0
+        X, ok = self.triangulate_dlt(rig.P0, rig.P1, x - s + st * m - st * d, x + s + st * m + st * d)
+        return X, bool(ok)
+
+    def compute_scene_points(self, result: FlowResult, rig: StereoRig) -> FlowResult:
+        """Fills points0/points1/scene_flow/point_valid from the dense s, m, d (geometry.hpp:54)."""
+        w, h = result.width, result.height
+        s, m, d = (np.ascontiguousarray(v, np.float64) for v in (result.s, result.m, result.d))
+        p0, p1, sf = (np.empty((h, w, 3)) for _ in range(3))
+        ok = np.empty((h, w), np.uint8)
+        rc = rig.to_c()
+        self.ctx.check(self.lib.hwf_scene_points(self.ctx.h, w, h, dptr(s), dptr(m), dptr(d), C.byref(rc), dptr(p0),
+                                                 dptr(p1), dptr(sf), u8ptr(ok)))
+        result.points0, result.points1, result.scene_flow, result.point_valid = p0, p1, sf, ok
+        result.has_points = True
+        return result
+
+    def export_mesh_obj(self, result: FlowResult, path: str | Path) -> None:
+        """geometry.hpp:56-59: OBJ over the pixel grid (3D points when present, else (x, y, disparity))."""
+        vis = np.ascontiguousarray(result.vis4, np.uint8)
+        disp = None if result.disparity is None else np.ascontiguousarray(result.disparity, np.float64)
+        pts = np.ascontiguousarray(result.points0, np.float64) if result.has_points else None
+        ok = np.ascontiguousarray(result.point_valid, np.uint8) if result.has_points else None
+        self.ctx.check(self.lib.hwf_export_mesh_obj(self.ctx.h, result.width, result.height, dptr(disp), u8ptr(vis),
+                                                    dptr(pts), u8ptr(ok), str(path).encode()))
 
     def prolongate(self, wc, hc, wf, hf, step, total_c, vis_c=None, hm_c=None):
         gwf, ghf = grid_dims(wf, hf, step)
