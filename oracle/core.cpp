@@ -773,69 +773,85 @@ std::vector<Subdomain> build_subdomains(int gw, int gh, int step, int tile_px) {
   return kept;
 }
 
-// solver.cpp:414-482 — non-overlapping block-Jacobi sweeps with warm start.
-std::vector<double> schwarz(const System& S, const std::vector<Subdomain>& subs, int patch_iters,
-                            int pcg_iters) {
-  const int G = S.G();
-  std::vector<double> pub(6 * static_cast<size_t>(G), 0.0);
-  std::vector<int> owner(G, -1), loc(G, 0);
+// One sweep of schwarz_iterate (solver.cpp:430-480) over the subdomains s with take[s]
+// (all when take is null): each local PCG is warm-started from pub, with its off-subdomain
+// neighbours frozen at pub; the local solutions go to next.
+void schwarz_sweep(const System& S, const std::vector<Subdomain>& subs, const std::vector<int>& owner,
+                   const std::vector<int>& loc, const std::vector<double>& pub, std::vector<double>& next,
+                   int pcg_iters, const std::vector<char>* take) {
+  for (size_t s = 0; s < subs.size(); ++s) {
+    if (take && !(*take)[s]) continue;
+    const auto& in = subs[s].interior;
+    const int ln = static_cast<int>(in.size());
+    std::vector<double> b(6 * ln), x0(6 * ln);
+    for (int i = 0; i < ln; ++i) {
+      const int g = in[i];
+      double bi[6];
+      for (int c = 0; c < 6; ++c) bi[c] = S.rhs[6 * g + c];
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+          if (dx == 0 && dy == 0) continue;
+          const int nb = S.neighbor(g, dx, dy);
+          if (nb < 0 || owner[nb] == static_cast<int>(s)) continue;
+          const double* B = S.block(g, slot(dx, dy));
+          for (int r = 0; r < 6; ++r)
+            for (int c = 0; c < 6; ++c) bi[r] -= B[6 * r + c] * pub[6 * nb + c];
+        }
+      for (int c = 0; c < 6; ++c) {
+        b[6 * i + c] = bi[c];
+        x0[6 * i + c] = pub[6 * g + c];
+      }
+    }
+    auto apply = [&](const std::vector<double>& x, std::vector<double>& y) {
+      y.assign(6 * ln, 0.0);
+      for (int i = 0; i < ln; ++i) {
+        const int g = in[i];
+        for (int dy = -1; dy <= 1; ++dy)
+          for (int dx = -1; dx <= 1; ++dx) {
+            const int nb = S.neighbor(g, dx, dy);
+            if (nb < 0 || owner[nb] != static_cast<int>(s)) continue;
+            const double* B = S.block(g, slot(dx, dy));
+            for (int r = 0; r < 6; ++r)
+              for (int c = 0; c < 6; ++c) y[6 * i + r] += B[6 * r + c] * x[6 * loc[nb] + c];
+          }
+      }
+    };
+    auto precond = [&](const std::vector<double>& r, std::vector<double>& z) {
+      z.assign(6 * ln, 0.0);
+      for (int i = 0; i < ln; ++i)
+        for (int f = 0; f < 3; ++f) {
+          const double* M = &S.pre[(static_cast<size_t>(in[i]) * 3 + f) * 4];
+          const int o = 6 * i + 2 * f;
+          z[o] = M[0] * r[o] + M[1] * r[o + 1];
+          z[o + 1] = M[2] * r[o] + M[3] * r[o + 1];
+        }
+    };
+    const std::vector<double> xl = pcg_impl(apply, precond, b, x0, pcg_iters, nullptr);
+    for (int i = 0; i < ln; ++i)
+      for (int c = 0; c < 6; ++c) next[6 * in[i] + c] = xl[6 * i + c];
+  }
+}
+
+void subdomain_owner(const std::vector<Subdomain>& subs, int G, std::vector<int>& owner, std::vector<int>& loc) {
+  owner.assign(G, -1);
+  loc.assign(G, 0);
   for (size_t s = 0; s < subs.size(); ++s)
     for (size_t i = 0; i < subs[s].interior.size(); ++i) {
       owner[subs[s].interior[i]] = static_cast<int>(s);
       loc[subs[s].interior[i]] = static_cast<int>(i);
     }
+}
+
+// solver.cpp:414-482 — non-overlapping block-Jacobi sweeps with warm start.
+std::vector<double> schwarz(const System& S, const std::vector<Subdomain>& subs, int patch_iters,
+                            int pcg_iters) {
+  const int G = S.G();
+  std::vector<double> pub(6 * static_cast<size_t>(G), 0.0);
+  std::vector<int> owner, loc;
+  subdomain_owner(subs, G, owner, loc);
   for (int sweep = 0; sweep < patch_iters; ++sweep) {
     std::vector<double> next = pub;
-    for (size_t s = 0; s < subs.size(); ++s) {
-      const auto& in = subs[s].interior;
-      const int ln = static_cast<int>(in.size());
-      std::vector<double> b(6 * ln), x0(6 * ln);
-      for (int i = 0; i < ln; ++i) {
-        const int g = in[i];
-        double bi[6];
-        for (int c = 0; c < 6; ++c) bi[c] = S.rhs[6 * g + c];
-        for (int dy = -1; dy <= 1; ++dy)
-          for (int dx = -1; dx <= 1; ++dx) {
-            if (dx == 0 && dy == 0) continue;
-            const int nb = S.neighbor(g, dx, dy);
-            if (nb < 0 || owner[nb] == static_cast<int>(s)) continue;
-            const double* B = S.block(g, slot(dx, dy));
-            for (int r = 0; r < 6; ++r)
-              for (int c = 0; c < 6; ++c) bi[r] -= B[6 * r + c] * pub[6 * nb + c];
-          }
-        for (int c = 0; c < 6; ++c) {
-          b[6 * i + c] = bi[c];
-          x0[6 * i + c] = pub[6 * g + c];
-        }
-      }
-      auto apply = [&](const std::vector<double>& x, std::vector<double>& y) {
-        y.assign(6 * ln, 0.0);
-        for (int i = 0; i < ln; ++i) {
-          const int g = in[i];
-          for (int dy = -1; dy <= 1; ++dy)
-            for (int dx = -1; dx <= 1; ++dx) {
-              const int nb = S.neighbor(g, dx, dy);
-              if (nb < 0 || owner[nb] != static_cast<int>(s)) continue;
-              const double* B = S.block(g, slot(dx, dy));
-              for (int r = 0; r < 6; ++r)
-                for (int c = 0; c < 6; ++c) y[6 * i + r] += B[6 * r + c] * x[6 * loc[nb] + c];
-            }
-        }
-      };
-      auto precond = [&](const std::vector<double>& r, std::vector<double>& z) {
-        z.assign(6 * ln, 0.0);
-        for (int i = 0; i < ln; ++i)
-          for (int f = 0; f < 3; ++f) {
-            const double* M = &S.pre[(static_cast<size_t>(in[i]) * 3 + f) * 4];
-            const int o = 6 * i + 2 * f;
-            z[o] = M[0] * r[o] + M[1] * r[o + 1];
-            z[o + 1] = M[2] * r[o] + M[3] * r[o + 1];
-          }
-      };
-      const std::vector<double> xl = pcg_impl(apply, precond, b, x0, pcg_iters, nullptr);
-      for (int i = 0; i < ln; ++i)
-        for (int c = 0; c < 6; ++c) next[6 * in[i] + c] = xl[6 * i + c];
-    }
+    schwarz_sweep(S, subs, owner, loc, pub, next, pcg_iters, nullptr);
     pub = next;
   }
   return pub;

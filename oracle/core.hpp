@@ -132,6 +132,10 @@ struct Subdomain {
 std::vector<Subdomain> build_subdomains(int gw, int gh, int step, int tile_px);
 std::vector<double> schwarz(const System& S, const std::vector<Subdomain>& subs, int patch_iters,
                             int pcg_iters);
+void subdomain_owner(const std::vector<Subdomain>& subs, int G, std::vector<int>& owner, std::vector<int>& loc);
+void schwarz_sweep(const System& S, const std::vector<Subdomain>& subs, const std::vector<int>& owner,
+                   const std::vector<int>& loc, const std::vector<double>& pub, std::vector<double>& next,
+                   int pcg_iters, const std::vector<char>* take);
 
 // gauss_newton (solver.cpp:484-532). Level's total/delta/outlier/node_w are
 // rebound internally; delta, outlier and node_w are updated in place.

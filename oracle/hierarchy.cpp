@@ -35,6 +35,7 @@
 
 #include "backend.hpp"
 #include "ctx.hpp"
+#include "hierarchy.hpp"
 #include "hwflow_c.h"
 
 // Per-pair delta hierarchy + accumulated grids (SPEC.md:396 `prev`).
@@ -50,6 +51,8 @@ namespace {
 constexpr int kZbufSpanPx = 8;
 constexpr double kDepthTol = 1e-4;
 constexpr double kIllumSigma = 3.2;
+
+}  // namespace
 
 std::vector<std::vector<double>> load_frames(const hwf_frame4* f) {
   if (!f || f->width < 1 || f->height < 1) throw std::invalid_argument("bad frame dims");
@@ -69,8 +72,6 @@ std::vector<std::vector<double>> load_frames(const hwf_frame4* f) {
   }
   return out;
 }
-
-}  // namespace
 
 // ---- occlusion (pins C.2/C.3) -------------------------------
 void occlusion(int w, int h, int step, const double* total, uint8_t* vis4) {
@@ -260,12 +261,12 @@ void propagate(int w, int h, int step, const double* prev_delta, const double* p
   }
 }
 
-namespace {
-
 int gn_for_level(const hwf_schedule* S, int l) {  // solver.hpp:30-34
   if (S->n_gn_per_level > 0) return S->gn_per_level[std::min(l, S->n_gn_per_level - 1)];
   return l <= 1 ? 2 : 5;
 }
+
+namespace {
 
 // Algorithm 1.
 void run_scene_flow(Backend* B, const hwf_frame4* fr, const hwf_energy_params* P,

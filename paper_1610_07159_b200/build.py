@@ -22,7 +22,7 @@ ORACLE_DIR = ROOT / "oracle"
 ORACLE_LIB = ORACLE_DIR / "_build" / "libhwflow_oracle.so"
 REF_LIB = ORACLE_DIR / "_ref" / "libhwflow_ref.so"
 
-SOURCES = ["pixel.cu", "solve.cu", "maps.cu", "capi.cu", "stages.cu", "geometry.cu"]
+SOURCES = ["pixel.cu", "solve.cu", "maps.cu", "capi.cu", "stages.cu", "geometry.cu", "split.cu"]
 NVCC_FLAGS = [
     "-std=c++17", "-O3", "-lineinfo",
     "-gencode", "arch=compute_100a,code=sm_100a",

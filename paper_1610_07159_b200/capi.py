@@ -149,8 +149,27 @@ _EXT_SIGS = {
     "hwf_wait": (C.c_int, [C.c_void_p]),
 }
 
+_vpp = C.POINTER(C.c_void_p)
+_SPLIT_SIGS = {  # include/hwflow_split.h (both the CUDA library and the oracle)
+    "hwf_split_create": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(EnergyParamsC),
+                                   C.POINTER(ScheduleC), _dp, C.c_int, C.c_int, _vpp]),
+    "hwf_split_destroy": (None, [C.c_void_p]),
+    "hwf_split_schedule": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "hwf_split_rows": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "hwf_split_buffer": (C.c_int, [C.c_void_p, C.c_int, C.c_char_p, _vpp, C.POINTER(C.c_longlong)]),
+    "hwf_split_swept": (C.c_char_p, [C.c_int]),
+    "hwf_split_begin": (C.c_int, [C.c_void_p, C.POINTER(Frame4C)]),
+    "hwf_split_level_begin": (C.c_int, [C.c_void_p, C.c_int]),
+    "hwf_split_linearize": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
+    "hwf_split_sweep": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
+    "hwf_split_energy_after": (C.c_int, [C.c_void_p, C.c_int]),
+    "hwf_split_level_end": (C.c_int, [C.c_void_p, C.c_int]),
+    "hwf_split_finish": (C.c_int, [C.c_void_p, C.POINTER(ResultC), C.POINTER(StatsC)]),
+}
+
 EXPORTED = sorted(_SIGS)
 EXPORTED_EXT = sorted(_EXT_SIGS)
+EXPORTED_SPLIT = sorted(_SPLIT_SIGS)
 
 
 class Library:
@@ -160,6 +179,9 @@ class Library:
         self.path = Path(path)
         self.lib = C.CDLL(str(self.path))
         for name, (res, args) in _SIGS.items():
+            fn = getattr(self.lib, name)
+            fn.restype, fn.argtypes = res, args
+        for name, (res, args) in _SPLIT_SIGS.items():
             fn = getattr(self.lib, name)
             fn.restype, fn.argtypes = res, args
         self.has_ext = all(hasattr(self.lib, n) for n in _EXT_SIGS)

@@ -177,102 +177,133 @@ inline double pixel_bytes(const LevelDev& d, int B, bool illum, bool u8) {
   return B * (d.N * perpix + d.G * 48.0 + d.C * kCellStride * 8.0);
 }
 
-// The nonlinear loop of one level (solver.cpp:484-532) for a batch.
-// Pairs per chunk at a level. A GN iteration can run chunk by chunk (pixel ->
-// structw -> node -> sweeps) so one chunk's cell sums, system and Schwarz vectors
-// stay L2-resident between producer and consumer. Measured on B200 at cfg2,
-// B = 128 (profiles/r1_notes.md): 2/4/8/16/128-pair chunks -> 50.0/46.8/45.1/
-// 44.3/43.9 ms per batch, i.e. the whole batch per launch wins, so that is the
-// default; HWF_CHUNK_L0 (finest level, x4 per coarser level) keeps the knob.
-inline int level_chunk(const LevelDev& d, int B, int level) {
-  (void)d;
-  static const int env = [] {
-    const char* e = std::getenv("HWF_CHUNK_L0");
-    return e ? std::atoi(e) : 0;
-  }();
-  const int c = env > 0 ? env << (2 * level) : B;
-  return std::max(1, std::min(B, c));
+// Rows of one level a strip-split rank works on (hwflow_split.h); whole = the level.
+struct Range {
+  bool whole = true;
+  int pix0 = 0, pix1 = 0, pown0 = 0, pown1 = 0;      // pixel-tile rows computed / owning energies
+  int sw_lo = 0, sw_hi = 0;                          // k_structw nodes
+  int n_lo = 0, n_hi = 0, own_lo = 0, own_hi = 0;    // k_node nodes assembled / owning energies
+  int sub0 = 0, sub1 = 0;                            // Schwarz subdomains
+};
+
+inline PixArgs pixel_args(const LevelDev& d, const hwf_energy_params& P, const hwf_schedule& S, const uint8_t* src8,
+                          int* flags, const Energies& E, const Range* R) {
+  PixArgs pa{};
+  pa.w = d.w; pa.h = d.h; pa.gw = d.gw; pa.gh = d.gh; pa.step = d.step; pa.ncx = d.ncx; pa.ncy = d.ncy;
+  pa.tcx = d.tcx; pa.tcy = d.tcy; pa.rp = d.rp;
+  pa.pk = d.pk; pa.gy = d.gy; pa.src8 = src8; pa.illum = d.illum; pa.vis4 = d.vis; pa.W = d.W;
+  pa.total = d.total; pa.half = d.half; pa.cells = d.cells; pa.ep_pair = E.pair_stride(); pa.flags = flags;
+  pa.P = to_params(P); pa.active = S.active_fields;
+  if (R && !R->whole) {
+    pa.ty0 = R->pix0; pa.ty1 = R->pix1; pa.own0 = R->pown0; pa.own1 = R->pown1;
+  }
+  return pa;
 }
 
-// The nonlinear loop of one level (solver.cpp:484-532) for a batch.
+inline NodeArgs node_args(const LevelDev& d, const hwf_energy_params& P, const hwf_schedule& S, const double* dF,
+                          int* flags, const Energies& E, const Range* R) {
+  NodeArgs na{};
+  na.w = d.w; na.h = d.h; na.gw = d.gw; na.gh = d.gh; na.step = d.step; na.ncx = d.ncx; na.ncy = d.ncy;
+  na.half = d.half; na.node_w = d.nodew; na.node_w_new = d.nodew; na.total = d.total; na.delta = d.delta;
+  na.cells = d.cells; na.sys = d.sys; na.ep_pair = E.pair_stride(); na.ep_base = d.n_pix_cta; na.flags = flags;
+  na.P = to_params(P); na.F = dF; na.active = S.active_fields; na.lm = S.lm_lambda;
+  if (R && !R->whole) {
+    na.n_lo = R->n_lo; na.n_hi = R->n_hi; na.own_lo = R->own_lo; na.own_hi = R->own_hi;
+  }
+  return na;
+}
+
+// One Gauss-Newton linearisation (solver.cpp:497-511): refresh W and w_i, energies with the old
+// and new weights, J^T J / J^T r into the system. Leaves d.nodew pointing at the refreshed w_i.
+inline void rec_linearize(LevelDev& d, int B, const hwf_energy_params& P, const hwf_schedule& S, const double* dF,
+                          int it, const Energies& E, int slot_base, int* flags, cudaStream_t st, Launches& L,
+                          const uint8_t* src8, const Range* R = nullptr) {
+  double* wnew = d.nodew == d.nodew_a ? d.nodew_b : d.nodew_a;  // ping-pong w_i
+  PixArgs pa = pixel_args(d, P, S, src8, flags, E, R);
+  pa.refresh = 1;
+  pa.ep_new = E.slot(slot_base + 2 * it);
+  pa.ep_old = it > 0 ? E.slot(slot_base + 2 * (it - 1) + 1) : nullptr;
+  if (L.ev) CK(cudaEventRecordWithFlags((*L.ev)[2 * L.bytes->size()], st, cudaEventRecordExternal));
+  launch_pixel(true, pa, B, st);
+  if (L.ev) {
+    CK(cudaEventRecordWithFlags((*L.ev)[2 * L.bytes->size() + 1], st, cudaEventRecordExternal));
+    L.bytes->push_back(pixel_bytes(d, B, d.illum != nullptr, src8 != nullptr));
+  }
+  const bool whole = !R || R->whole;
+  launch_structw(d.w, d.h, d.gw, d.gh, d.step, d.half, wnew, B, st, whole ? 0 : R->sw_lo, whole ? -1 : R->sw_hi);
+  NodeArgs na = node_args(d, P, S, dF, flags, E, R);
+  na.node_w_new = wnew;
+  na.refresh = 1;
+  na.ep_new = pa.ep_new;
+  na.ep_old = pa.ep_old;
+  launch_node(true, na, B, st);
+  L.count += 3;
+  d.nodew = wnew;
+}
+
+// Sweep s of schwarz_iterate (solver.cpp:414-482); the last sweep applies the step.
+inline void rec_sweep(LevelDev& d, int B, const hwf_schedule& S, int s, int* flags, cudaStream_t st, Launches& L,
+                      const Range* R = nullptr) {
+  SwzArgs sa{};
+  sa.gw = d.gw; sa.gh = d.gh; sa.step = d.step; sa.tile = d.tile; sa.ntx = d.ntx; sa.nty = d.nty;
+  sa.nxm = d.nxm; sa.nym = d.nym; sa.sys = d.sys; sa.delta = d.delta; sa.total = d.total;
+  sa.base = d.base; sa.active = S.active_fields; sa.pcg_iters = S.pcg_iters; sa.flags = flags;
+  sa.pub = s == 0 ? nullptr : (s & 1 ? d.xb : d.xa);
+  sa.next = s & 1 ? d.xa : d.xb;
+  sa.last = s == S.patch_iters - 1;
+  if (R && !R->whole) {
+    sa.sub0 = R->sub0;
+    sa.sub1 = R->sub1;
+  }
+  launch_schwarz(sa, B, st);
+  L.count += 1;
+}
+// The buffer sweep s publishes (read by sweep s + 1).
+inline double* swept(LevelDev& d, int s) { return s & 1 ? d.xa : d.xb; }
+
+// E_after of the last iteration (solver.cpp:523-528).
+inline void rec_energy_after(LevelDev& d, int B, const hwf_energy_params& P, const hwf_schedule& S, const double* dF,
+                             int gn, const Energies& E, int slot_base, int* flags, cudaStream_t st, Launches& L,
+                             const uint8_t* src8, const Range* R = nullptr) {
+  PixArgs pa = pixel_args(d, P, S, src8, flags, E, R);
+  pa.refresh = 0;
+  pa.ep_new = E.slot(slot_base + 2 * (gn - 1) + 1);
+  pa.ep_old = nullptr;
+  if (R && !R->whole) {  // energies only: the owned rows
+    pa.ty0 = R->pown0;
+    pa.ty1 = R->pown1;
+  }
+  launch_pixel(false, pa, B, st);
+  NodeArgs na = node_args(d, P, S, dF, flags, E, R);
+  if (R && !R->whole) {
+    na.n_lo = R->own_lo;
+    na.n_hi = R->own_hi;
+  }
+  na.refresh = 0;
+  na.ep_new = pa.ep_new;
+  na.ep_old = nullptr;
+  launch_node(false, na, B, st);
+  L.count += 2;
+}
+
+// The nonlinear loop of one level (solver.cpp:484-532) for a batch, whole level.
 inline void record_gn_level(LevelDev& d, int B, const hwf_energy_params& P, const hwf_schedule& S, const double* dF,
-                     int gn, const Energies& E, int slot_base, Scratch& sc, int* flags, cudaStream_t st,
-                     Launches& L, int chunk = 0, const uint8_t* src8 = nullptr) {
-  const int CH = chunk > 0 ? std::min(chunk, B) : B;
-  const long long eps = E.pair_stride();
+                            int gn, const Energies& E, int slot_base, Scratch& sc, int* flags, cudaStream_t st,
+                            Launches& L, const uint8_t* src8 = nullptr) {
   for (int it = 0; it < gn; ++it) {
-    double* wnew = d.nodew == d.nodew_a ? d.nodew_b : d.nodew_a;  // ping-pong w_i
-    for (int c0 = 0; c0 < B; c0 += CH) {
-      const int bc = std::min(CH, B - c0);
-      const size_t pN = static_cast<size_t>(c0) * d.N, pG = static_cast<size_t>(c0) * d.G;
-      PixArgs pa{};
-      pa.w = d.w; pa.h = d.h; pa.gw = d.gw; pa.gh = d.gh; pa.step = d.step; pa.ncx = d.ncx; pa.ncy = d.ncy;
-      pa.tcx = d.tcx; pa.tcy = d.tcy; pa.rp = d.rp;
-      pa.pk = d.pk + 4 * pN; pa.gy = d.gy + 4 * pN; pa.src8 = src8 ? src8 + 4 * pN : nullptr; pa.illum = d.illum ? d.illum + 4 * pN : nullptr;
-      pa.vis4 = d.vis + pN; pa.W = d.W + pN; pa.total = d.total + 6 * pG; pa.half = d.half + pN;
-      pa.cells = d.cells + static_cast<size_t>(c0) * d.C * kCellStride; pa.ep_pair = eps; pa.flags = flags + c0;
-      pa.P = to_params(P); pa.active = S.active_fields; pa.refresh = 1;
-      pa.ep_new = E.slot(slot_base + 2 * it) + c0 * eps;
-      pa.ep_old = it > 0 ? E.slot(slot_base + 2 * (it - 1) + 1) + c0 * eps : nullptr;
-      if (L.ev) CK(cudaEventRecordWithFlags((*L.ev)[2 * L.bytes->size()], st, cudaEventRecordExternal));
-      launch_pixel(true, pa, bc, st);
-      if (L.ev) {
-        CK(cudaEventRecordWithFlags((*L.ev)[2 * L.bytes->size() + 1], st, cudaEventRecordExternal));
-        L.bytes->push_back(pixel_bytes(d, bc, d.illum != nullptr, src8 != nullptr));
-      }
-      launch_structw(d.w, d.h, d.gw, d.gh, d.step, d.half + pN, wnew + pG, bc, st);
-      NodeArgs na{};
-      na.w = d.w; na.h = d.h; na.gw = d.gw; na.gh = d.gh; na.step = d.step; na.ncx = d.ncx; na.ncy = d.ncy;
-      na.half = d.half + pN; na.node_w = d.nodew + pG; na.node_w_new = wnew + pG; na.total = d.total + 6 * pG;
-      na.delta = d.delta + 6 * pG; na.cells = pa.cells; na.sys = d.sys + static_cast<size_t>(kSysStride) * pG;
-      na.ep_pair = eps; na.ep_base = d.n_pix_cta; na.flags = flags + c0; na.P = to_params(P); na.F = dF;
-      na.active = S.active_fields; na.lm = S.lm_lambda; na.refresh = 1; na.ep_new = pa.ep_new; na.ep_old = pa.ep_old;
-      launch_node(true, na, bc, st);
-      L.count += 3;
-      if (S.subdomain_px > 0) {
-        SwzArgs sa{};
-        sa.gw = d.gw; sa.gh = d.gh; sa.step = d.step; sa.tile = d.tile; sa.ntx = d.ntx; sa.nty = d.nty;
-        sa.nxm = d.nxm; sa.nym = d.nym; sa.sys = na.sys; sa.delta = d.delta + 6 * pG; sa.total = d.total + 6 * pG;
-        sa.base = d.base + 6 * pG; sa.active = S.active_fields; sa.pcg_iters = S.pcg_iters; sa.flags = flags + c0;
-        for (int s = 0; s < S.patch_iters; ++s) {
-          sa.pub = s == 0 ? nullptr : (s & 1 ? d.xb : d.xa) + 6 * pG;
-          sa.next = (s & 1 ? d.xa : d.xb) + 6 * pG;
-          sa.last = s == S.patch_iters - 1;
-          launch_schwarz(sa, bc, st);
-          L.count += 1;
-        }
-      } else {
-        PcgArgs ga{};
-        ga.gw = d.gw; ga.gh = d.gh; ga.iters = S.pcg_iters; ga.sys = na.sys;
-        ga.x = sc.px + 6 * pG; ga.r = sc.pr + 6 * pG; ga.z = sc.pz + 6 * pG; ga.p = sc.pp + 6 * pG;
-        ga.ap = sc.pap + 6 * pG; ga.trace = nullptr; ga.update = 1; ga.delta = d.delta + 6 * pG;
-        ga.total = d.total + 6 * pG; ga.base = d.base + 6 * pG; ga.active = S.active_fields; ga.flags = flags + c0;
-        launch_pcg_global(ga, bc, st);
-        L.count += 1;
-      }
+    rec_linearize(d, B, P, S, dF, it, E, slot_base, flags, st, L, src8);
+    if (S.subdomain_px > 0) {
+      for (int s = 0; s < S.patch_iters; ++s) rec_sweep(d, B, S, s, flags, st, L);
+    } else {
+      PcgArgs ga{};
+      ga.gw = d.gw; ga.gh = d.gh; ga.iters = S.pcg_iters; ga.sys = d.sys;
+      ga.x = sc.px; ga.r = sc.pr; ga.z = sc.pz; ga.p = sc.pp; ga.ap = sc.pap; ga.trace = nullptr; ga.update = 1;
+      ga.delta = d.delta; ga.total = d.total; ga.base = d.base; ga.active = S.active_fields; ga.flags = flags;
+      launch_pcg_global(ga, B, st);
+      L.count += 1;
     }
-    d.nodew = wnew;
   }
-  if (gn > 0) {  // E_after of the last iteration (solver.cpp:523-528), whole batch
-    PixArgs pa{};
-    pa.w = d.w; pa.h = d.h; pa.gw = d.gw; pa.gh = d.gh; pa.step = d.step; pa.ncx = d.ncx; pa.ncy = d.ncy;
-    pa.tcx = d.tcx; pa.tcy = d.tcy; pa.rp = d.rp;
-    pa.pk = d.pk; pa.gy = d.gy; pa.src8 = src8; pa.illum = d.illum; pa.vis4 = d.vis; pa.W = d.W; pa.total = d.total; pa.half = d.half;
-    pa.cells = d.cells; pa.ep_pair = eps; pa.flags = flags; pa.P = to_params(P); pa.active = S.active_fields;
-    pa.refresh = 0;
-    pa.ep_new = E.slot(slot_base + 2 * (gn - 1) + 1);
-    pa.ep_old = nullptr;
-    launch_pixel(false, pa, B, st);
-    NodeArgs na{};
-    na.w = d.w; na.h = d.h; na.gw = d.gw; na.gh = d.gh; na.step = d.step; na.ncx = d.ncx; na.ncy = d.ncy;
-    na.half = d.half; na.node_w = d.nodew; na.node_w_new = d.nodew; na.total = d.total; na.delta = d.delta;
-    na.cells = d.cells; na.sys = d.sys; na.ep_pair = eps; na.ep_base = d.n_pix_cta; na.flags = flags;
-    na.P = to_params(P); na.F = dF; na.active = S.active_fields; na.lm = S.lm_lambda; na.refresh = 0;
-    na.ep_new = pa.ep_new;
-    na.ep_old = nullptr;
-    launch_node(false, na, B, st);
-    L.count += 2;
-  }
+  if (gn > 0) rec_energy_after(d, B, P, S, dF, gn, E, slot_base, flags, st, L, src8);
 }
 
 // ---- the batched plan (one CUDA graph per configuration) ------------------------
@@ -385,6 +416,23 @@ struct Plan {
   }
 
   void build(cudaStream_t st) {
+    alloc();
+    // capture the pipeline into one graph
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    try {
+      record(st);
+    } catch (...) {
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(st, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    CK(cudaStreamEndCapture(st, &graph));
+    CK(cudaGraphInstantiate(&exec, graph, 0));
+  }
+
+  // Level dims, schedule and every device buffer of the plan (no capture).
+  void alloc() {
     int dims[4 * HWF_MAX_LEVELS];
     if (hwf_level_dims(w, h, S.levels, S.grid_step, &L, dims) != HWF_OK) throw InvalidArg("bad level dims");
     size_t cap = 0;
@@ -431,26 +479,13 @@ struct Plan {
     if (outmask & 8) o_disp = mem.alloc<double>(B * N0);
     if (profile) {
       int total_gn = 0;
-      for (int l = 0; l < L; ++l) {
-        const int ch = level_chunk(lv[l], B, l);
-        total_gn += gn[l] * ((B + ch - 1) / ch);
-      }
+      for (int l = 0; l < L; ++l) total_gn += gn[l];
       ev.resize(2 * std::max(total_gn, 1));
       for (auto& e : ev) CK(cudaEventCreate(&e));
     }
-    // capture the pipeline into one graph
-    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    try {
-      record(st);
-    } catch (...) {
-      cudaGraph_t g = nullptr;
-      cudaStreamEndCapture(st, &g);
-      if (g) cudaGraphDestroy(g);
-      throw;
-    }
-    CK(cudaStreamEndCapture(st, &graph));
-    CK(cudaGraphInstantiate(&exec, graph, 0));
   }
+
+  const uint8_t* src8(int l) const { return u8_finest(l) ? static_cast<const uint8_t*>(in) : nullptr; }
 
   void record(cudaStream_t st) {
     Launches LC;
@@ -459,6 +494,18 @@ struct Plan {
       LC.ev = &ev;
       LC.bytes = &ev_bytes;
     }
+    rec_prologue(st, LC);
+    for (int l = L - 1; l >= 0; --l) {
+      rec_level_begin(l, st, LC);
+      record_gn_level(lv[l], B, P, S, dF, gn[l], E, slot_base[l], sc, flags, st, LC, src8(l));
+      rec_level_end(l, st, LC);
+    }
+    rec_epilogue(st, LC);
+    launches = LC.count;
+  }
+
+  // energy/flag reset, pyramid (image.cpp:177-185), sample planes
+  void rec_prologue(cudaStream_t st, Launches& LC) {
     CK(cudaMemsetAsync(E.part, 0, sizeof(double) * B * E.pair_stride(), st));
     CK(cudaMemsetAsync(flags, 0, sizeof(int) * B, st));
     // pyramid (image.cpp:177-185)
@@ -473,35 +520,44 @@ struct Plan {
       launch_pack(lv[l].img, lv[l].w, lv[l].h, 4 * B, lv[l].pk, lv[l].gy, st);
       LC.count++;
     }
-    for (int l = L - 1; l >= 0; --l) {
-      LevelDev& d = lv[l];
-      if (l == L - 1) {  // pin C.6
-        launch_init_coarse(d.base, d.total, d.delta, static_cast<int>(d.G), B, S.coarse_s_offset[0],
-                           S.coarse_s_offset[1], st);
-        CK(cudaMemsetAsync(d.vis, 0x0F, B * d.N, st));
-        LC.count++;
-      } else {  // prolongation
-        const LevelDev& c = lv[l + 1];
-        launch_prolong_grid(c.gw, c.gh, d.gw, d.gh, d.step, c.total, d.base, d.total, d.delta, B, st);
-        launch_prolong_maps(c.w, c.h, d.w, d.h, c.occ, c.hm, d.vis, d.illum, B, st);
-        LC.count += 2;
-      }
-      if (has_prev) {  // warm start: delta_l = advected previous delta
-        launch_propagate(d.gw, d.gh, d.step, prev_delta[l], prev_total[l], d.base, d.delta, d.total, B, st);
-        LC.count++;
-      }
-      CK(cudaMemsetAsync(d.W, 1, B * d.N, st));
-      CK(cudaMemsetAsync(d.nodew, 0, sizeof(double) * B * d.G, st));
-      record_gn_level(d, B, P, S, dF, gn[l], E, slot_base[l], sc, flags, st, LC, level_chunk(d, B, l),
-                      u8_finest(l) ? static_cast<const uint8_t*>(in) : nullptr);
-      launch_occlusion(d.w, d.h, d.gw, d.gh, d.step, d.total, B, sc.q, sc.Z, sc.bad, sc.zbuf, sc.degen, sc.queue,
-                       sc.qcount, d.occ, st);
-      LC.count += 4;
-      if (l > 0) {
-        launch_illumination(d.w, d.h, d.gw, d.gh, d.step, d.img, d.total, d.occ, B, sc.resid, sc.tmp, d.hm, st);
-        LC.count += 3;
-      }
+  }
+
+  // coarsest init (pin C.6) or prolongation, warm start, W / w_i reset
+  void rec_level_begin(int l, cudaStream_t st, Launches& LC) {
+    LevelDev& d = lv[l];
+    if (l == L - 1) {  // pin C.6
+      launch_init_coarse(d.base, d.total, d.delta, static_cast<int>(d.G), B, S.coarse_s_offset[0],
+                         S.coarse_s_offset[1], st);
+      CK(cudaMemsetAsync(d.vis, 0x0F, B * d.N, st));
+      LC.count++;
+    } else {  // prolongation
+      const LevelDev& c = lv[l + 1];
+      launch_prolong_grid(c.gw, c.gh, d.gw, d.gh, d.step, c.total, d.base, d.total, d.delta, B, st);
+      launch_prolong_maps(c.w, c.h, d.w, d.h, c.occ, c.hm, d.vis, d.illum, B, st);
+      LC.count += 2;
     }
+    if (has_prev) {  // warm start: delta_l = advected previous delta
+      launch_propagate(d.gw, d.gh, d.step, prev_delta[l], prev_total[l], d.base, d.delta, d.total, B, st);
+      LC.count++;
+    }
+    CK(cudaMemsetAsync(d.W, 1, B * d.N, st));
+    CK(cudaMemsetAsync(d.nodew, 0, sizeof(double) * B * d.G, st));
+  }
+
+  // occlusion and illumination of the solved level
+  void rec_level_end(int l, cudaStream_t st, Launches& LC) {
+    LevelDev& d = lv[l];
+    launch_occlusion(d.w, d.h, d.gw, d.gh, d.step, d.total, B, sc.q, sc.Z, sc.bad, sc.zbuf, sc.degen, sc.queue,
+                     sc.qcount, d.occ, st);
+    LC.count += 4;
+    if (l > 0) {
+      launch_illumination(d.w, d.h, d.gw, d.gh, d.step, d.img, d.total, d.occ, B, sc.resid, sc.tmp, d.hm, st);
+      LC.count += 3;
+    }
+  }
+
+  // dense FlowResult (pin C.7) and the per-slot energy reduction
+  void rec_epilogue(cudaStream_t st, Launches& LC) {
     if (outmask & 15) {
       launch_dense(lv[0].w, lv[0].h, lv[0].gw, lv[0].gh, lv[0].step, lv[0].total, B, o_s, o_m, o_d, o_disp, st);
       LC.count++;
@@ -509,7 +565,6 @@ struct Plan {
     launch_energy_reduce(E.part, E.nslots, E.cap, B, E.red, flags, st);
     LC.count++;
     CK(cudaGetLastError());
-    launches = LC.count;
   }
 };
 

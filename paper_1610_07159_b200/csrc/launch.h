@@ -36,6 +36,9 @@ struct PixArgs {
   uint32_t active;
   int refresh;
   double* resid;        // optional stacked R (energy.cpp:208-228): photo [0,N), grad [N,2N)
+  // strip split (hwflow_split.h): pixel-tile rows [ty0, ty1) are computed, rows [own0, own1)
+  // contribute energy partials (others write zeros); ty1 <= 0 = the whole level
+  int ty0, ty1, own0, own1;
 };
 
 struct NodeArgs {
@@ -59,6 +62,9 @@ struct NodeArgs {
   int refresh;
   double* resid;        // optional stacked R: smooth [2N,2N+6G), epi [..+2G), mag [..+6G)
   long long resid_n;    // N of the level (offset of the node blocks)
+  // strip split: nodes [n_lo, n_hi) are assembled, nodes [own_lo, own_hi) contribute energy
+  // partials; n_hi <= 0 = the whole level
+  int n_lo, n_hi, own_lo, own_hi;
 };
 
 struct SwzArgs {
@@ -73,6 +79,7 @@ struct SwzArgs {
   uint32_t active;
   int pcg_iters;
   int* flags;
+  int sub0, sub1;       // strip split: subdomains [sub0, sub1); sub1 <= 0 = all
 };
 
 struct PcgArgs {
@@ -102,7 +109,7 @@ void launch_pack(const double* img, int w, int h, int planes, double2* pk, doubl
 int node_ctas(int G);
 void launch_node(bool lin, const NodeArgs& a, int B, cudaStream_t s);
 void launch_structw(int w, int h, int gw, int gh, int step, const double* half, double* wout, int B,
-                    cudaStream_t s);
+                    cudaStream_t s, int n_lo = 0, int n_hi = -1);
 
 // solve.cu
 void launch_schwarz(const SwzArgs& a, int B, cudaStream_t s);

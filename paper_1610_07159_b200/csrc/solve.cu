@@ -50,9 +50,9 @@ __global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM) k_schwarz(const SwzAr
   __shared__ double scratch[TEAM / 32 + 1];
   const int team = threadIdx.x / TEAM, u = threadIdx.x % TEAM;
   const int pair = blockIdx.y;
-  const int sub = blockIdx.x * SUBS + team;
+  const int sub = a.sub0 + blockIdx.x * SUBS + team;
   const int G = a.gw * a.gh;
-  const bool sub_ok = sub < a.ntx * a.nty;
+  const bool sub_ok = sub < a.sub1;
   const int tx = sub_ok ? sub % a.ntx : 0, ty = sub_ok ? sub / a.ntx : 0;
   const int alo = (tx * a.tile + a.step - 1) / a.step, ahi = min(a.gw - 1, ((tx + 1) * a.tile - 1) / a.step);
   const int blo = (ty * a.tile + a.step - 1) / a.step, bhi = min(a.gh - 1, ((ty + 1) * a.tile - 1) / a.step);
@@ -313,8 +313,14 @@ __global__ void __launch_bounds__(kPcgThreads) k_pcg_global(const PcgArgs a) {
 
 }  // namespace
 
-void launch_schwarz(const SwzArgs& a, int B, cudaStream_t s) {
-  const int nsub = a.ntx * a.nty;
+void launch_schwarz(const SwzArgs& a_in, int B, cudaStream_t s) {
+  SwzArgs a = a_in;
+  if (a.sub1 <= 0) {  // whole level
+    a.sub0 = 0;
+    a.sub1 = a.ntx * a.nty;
+  }
+  const int nsub = a.sub1 - a.sub0;
+  if (nsub <= 0) return;
   const int nodes = a.nxm * a.nym;
   if (nodes <= 4) {
     k_schwarz<32, 4><<<dim3((nsub + 3) / 4, B), 128, 0, s>>>(a);

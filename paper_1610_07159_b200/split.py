@@ -1,0 +1,301 @@
+"""Strip-split solve of one frame pair across ranks (SURVEY.md §8e, 4K mode).
+
+The C side is include/hwflow_split.h. This file is the driver that sequences its steps and
+moves data between ranks.
+  - The product (libhwflow_cuda.so): one rank per GPU, `TorchComm` over NCCL.
+  - The CPU tests: the oracle (host buffers) on gloo ranks, or on in-process `LocalComm`
+    ranks that copy rows directly.
+Collectives and data movement per frame:
+  - After every Schwarz sweep but the last: halo exchange of the published x rows next to
+    each strip (P2P), 2 node rows per rank.
+  - After every Gauss-Newton iteration: all-gather of the owned total/delta rows. Occlusion,
+    illumination, prolongation and the next linearisation read the whole grid.
+  - At the end: sum-all-reduce of the energy partials and OR of the divergence flags.
+Schwarz sweeps are Jacobi across subdomains (solver.cpp:430-480), so a split with exact
+halos reproduces the unsplit solve bit for bit.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .capi import DTYPE_F64, DTYPE_U8, Frame4C, ResultC, StatsC, dptr, u8ptr
+from .hwflow import EnergyParams, FlowResult, GnStats, SolveSchedule, Solver, grid_dims
+
+__all__ = ["SplitRank", "LocalComm", "TorchComm", "solve_split"]
+
+
+class _DevArray:  # zero-copy view of library-owned device memory for torch
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 2}
+
+
+class SplitRank:
+    """One rank's hwf_split: device buffers (CUDA library) or host buffers (oracle)."""
+
+    def __init__(self, solver: Solver, width: int, height: int, dtype: int, params: EnergyParams,
+                 schedule: SolveSchedule, fundamental: np.ndarray | None, rank: int, world: int):
+        self.solver, self.lib, self.rank, self.world = solver, solver.lib, rank, world
+        self.on_device = solver.backend.startswith("cuda")
+        self.width, self.height, self.dtype = width, height, dtype
+        self._pc, self._sc = params.to_c(), schedule.to_c()
+        self._F = None if fundamental is None else np.ascontiguousarray(fundamental, np.float64).reshape(9)
+        h = C.c_void_p()
+        self._check(self.lib.hwf_split_create(solver.ctx.h, width, height, dtype, C.byref(self._pc),
+                                              C.byref(self._sc), dptr(self._F), rank, world, C.byref(h)))
+        self.h = h
+        L, gn = C.c_int(), (C.c_int * 8)()
+        self._check(self.lib.hwf_split_schedule(self.h, C.byref(L), gn))
+        self.levels, self.gn = L.value, [gn[l] for l in range(L.value)]
+        self.patch_iters = schedule.patch_iters
+        self.rows = []  # per level: (n0, n1, gw)
+        for l in range(self.levels):
+            n0, n1, gw = C.c_int(), C.c_int(), C.c_int()
+            self._check(self.lib.hwf_split_rows(self.h, l, C.byref(n0), C.byref(n1), C.byref(gw)))
+            self.rows.append((n0.value, n1.value, gw.value))
+        self.stream = (torch.cuda.ExternalStream(self.lib.hwf_stream(solver.ctx.h)) if self.on_device else None)
+
+    def _check(self, rc: int):
+        self.solver.ctx.check(rc)
+
+    def buffer(self, level: int, name: str) -> torch.Tensor:
+        p, n = C.c_void_p(), C.c_longlong()
+        self._check(self.lib.hwf_split_buffer(self.h, level, name.encode(), C.byref(p), C.byref(n)))
+        flags = name == "flags"
+        if self.on_device:
+            return torch.as_tensor(_DevArray(p.value, n.value, "<i4" if flags else "<f8"), device="cuda")
+        ct = C.c_int32 if flags else C.c_double
+        return torch.from_numpy(np.ctypeslib.as_array(C.cast(p, C.POINTER(ct)), shape=(n.value,)))
+
+    def row_slice(self, level: int, r0: int, r1: int) -> slice:
+        gw = self.rows[level][2]
+        return slice(6 * gw * r0, 6 * gw * r1)
+
+    # steps (include/hwflow_split.h)
+    def begin(self, frame: Frame4C):
+        self._check(self.lib.hwf_split_begin(self.h, C.byref(frame)))
+
+    def level_begin(self, l: int):
+        self._check(self.lib.hwf_split_level_begin(self.h, l))
+
+    def linearize(self, l: int, it: int):
+        self._check(self.lib.hwf_split_linearize(self.h, l, it))
+
+    def sweep(self, l: int, s: int):
+        self._check(self.lib.hwf_split_sweep(self.h, l, s))
+
+    def energy_after(self, l: int):
+        self._check(self.lib.hwf_split_energy_after(self.h, l))
+
+    def level_end(self, l: int):
+        self._check(self.lib.hwf_split_level_end(self.h, l))
+
+    def finish(self) -> tuple[FlowResult, GnStats]:
+        w, h = self.width, self.height
+        gw, gh = grid_dims(w, h, self._sc.grid_step)
+        o = FlowResult(w, h)
+        o.s, o.m, o.d = np.empty((h, w, 2)), np.empty((h, w, 2)), np.empty((h, w, 2))
+        o.disparity, o.vis4, o.grid_total = np.empty((h, w)), np.empty((h, w), np.uint8), np.empty((gw * gh, 6))
+        r = ResultC(dptr(o.s), dptr(o.m), dptr(o.d), dptr(o.disparity), u8ptr(o.vis4), dptr(o.grid_total))
+        st = StatsC()
+        self._check(self.lib.hwf_split_finish(self.h, C.byref(r), C.byref(st)))
+        return o, GnStats.from_c(st)
+
+    def close(self):
+        if self.h:
+            self.lib.hwf_split_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _owner(rows: list[tuple[int, int]], q: int) -> int:
+    for r, (n0, n1) in enumerate(rows):
+        if n0 <= q < n1:
+            return r
+    raise ValueError(f"node row {q} has no owner")
+
+
+class LocalComm:
+    """All ranks in this process (oracle on CPU, or several splits sharing one device context):
+    rows move by direct copies, in step order."""
+
+    def _streamed(self, ranks):
+        s = ranks[0].stream
+        return torch.cuda.stream(s) if s is not None else _Null()
+
+    def halo(self, ranks: list[SplitRank], level: int, name: str):
+        rows = [r.rows[level][:2] for r in ranks]
+        gh = max(n1 for _, n1 in rows)
+        with self._streamed(ranks):
+            for r, (n0, n1) in zip(ranks, rows):
+                if n1 <= n0:
+                    continue
+                for q in (n0 - 1, n1):
+                    if 0 <= q < gh:
+                        src = ranks[_owner(rows, q)]
+                        sl = r.row_slice(level, q, q + 1)
+                        r.buffer(level, name)[sl].copy_(src.buffer(level, name)[sl])
+
+    def allgather_rows(self, ranks: list[SplitRank], level: int, name: str):
+        with self._streamed(ranks):
+            for src in ranks:
+                n0, n1, _ = src.rows[level]
+                if n1 <= n0:
+                    continue
+                sl = src.row_slice(level, n0, n1)
+                for dst in ranks:
+                    if dst is not src:
+                        dst.buffer(level, name)[sl].copy_(src.buffer(level, name)[sl])
+
+    def allreduce_sum(self, ranks: list[SplitRank], name: str):
+        with self._streamed(ranks):
+            bufs = [r.buffer(0, name) for r in ranks]
+            tot = bufs[0].clone()
+            for b in bufs[1:]:
+                tot += b
+            for b in bufs:
+                b.copy_(tot)
+
+    def allreduce_or(self, ranks: list[SplitRank], name: str):
+        with self._streamed(ranks):
+            bufs = [r.buffer(0, name) for r in ranks]
+            acc = bufs[0].clone()
+            for b in bufs[1:]:
+                acc |= b
+            for b in bufs:
+                b.copy_(acc)
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+class TorchComm:
+    """One rank per process over torch.distributed (NCCL for device buffers, gloo for host buffers)."""
+
+    def __init__(self, rank: SplitRank, group=None):
+        self.group = group
+        self.world = dist.get_world_size(group)
+        me = torch.tensor([v for (n0, n1, _) in rank.rows for v in (n0, n1)], dtype=torch.int64)
+        dev = "cuda" if rank.on_device else "cpu"
+        gathered = torch.empty(self.world * me.numel(), dtype=torch.int64, device=dev)
+        dist.all_gather_into_tensor(gathered, me.to(dev), group=group)
+        self.table = gathered.view(self.world, -1, 2).cpu().tolist()  # [rank][level][n0, n1]
+
+    def _streamed(self, ranks):
+        s = ranks[0].stream
+        return torch.cuda.stream(s) if s is not None else _Null()
+
+    def halo(self, ranks: list[SplitRank], level: int, name: str):
+        (me,) = ranks
+        rows = [self.table[r][level] for r in range(self.world)]
+        gh = max(n1 for _, n1 in rows)
+        buf = me.buffer(level, name)
+        ops = []
+        for r, (n0, n1) in enumerate(rows):
+            if n1 <= n0 or r == me.rank:
+                continue
+            for tag, q in ((0, n0 - 1), (1, n1)):
+                if 0 <= q < gh and _owner(rows, q) == me.rank:  # r needs my row q
+                    ops.append(dist.P2POp(dist.isend, buf[me.row_slice(level, q, q + 1)], r, self.group, tag))
+        n0, n1 = rows[me.rank]
+        if n1 > n0:
+            for tag, q in ((0, n0 - 1), (1, n1)):
+                if 0 <= q < gh:
+                    ops.append(dist.P2POp(dist.irecv, buf[me.row_slice(level, q, q + 1)], _owner(rows, q),
+                                          self.group, tag))
+        if not ops:
+            return
+        with self._streamed(ranks):
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def allgather_rows(self, ranks: list[SplitRank], level: int, name: str):
+        (me,) = ranks
+        rows = [self.table[r][level] for r in range(self.world)]
+        gw = me.rows[level][2]
+        span = 6 * gw * max(n1 - n0 for n0, n1 in rows)
+        if span == 0:
+            return
+        buf = me.buffer(level, name)
+        with self._streamed(ranks):
+            n0, n1 = rows[me.rank]
+            slab = torch.zeros(span, dtype=buf.dtype, device=buf.device)
+            slab[: 6 * gw * (n1 - n0)].copy_(buf[me.row_slice(level, n0, n1)])
+            out = torch.empty(self.world * span, dtype=buf.dtype, device=buf.device)
+            dist.all_gather_into_tensor(out, slab, group=self.group)
+            for r, (a, b) in enumerate(rows):
+                if r != me.rank and b > a:
+                    buf[me.row_slice(level, a, b)].copy_(out[r * span: r * span + 6 * gw * (b - a)])
+
+    def allreduce_sum(self, ranks: list[SplitRank], name: str):
+        (me,) = ranks
+        with self._streamed(ranks):
+            dist.all_reduce(me.buffer(0, name), op=dist.ReduceOp.SUM, group=self.group)
+
+    def allreduce_or(self, ranks: list[SplitRank], name: str):
+        (me,) = ranks
+        buf = me.buffer(0, name)
+        with self._streamed(ranks):
+            out = torch.empty(self.world * buf.numel(), dtype=buf.dtype, device=buf.device)
+            dist.all_gather_into_tensor(out, buf.clone(), group=self.group)
+            acc = out.view(self.world, -1)[0].clone()
+            for r in range(1, self.world):
+                acc |= out.view(self.world, -1)[r]
+            buf.copy_(acc)
+
+
+def _frame(images: np.ndarray) -> tuple[Frame4C, np.ndarray]:
+    a = np.ascontiguousarray(images)
+    if a.dtype != np.uint8:
+        a = np.ascontiguousarray(a, dtype=np.float64)
+    f = Frame4C()
+    f.width, f.height = a.shape[2], a.shape[1]
+    f.dtype = DTYPE_U8 if a.dtype == np.uint8 else DTYPE_F64
+    for e in range(4):
+        f.plane[e] = a[e].ctypes.data
+    return f, a
+
+
+def solve_split(ranks: list[SplitRank], comm, images: np.ndarray) -> list[tuple[FlowResult, GnStats]]:
+    """run_scene_flow of one frame pair (4, h, w), split across `ranks`
+    (all of them for LocalComm, this process's one for TorchComm). Returns each local rank's
+    (FlowResult, GnStats); every rank ends with the full result."""
+    frame, keep = _frame(images)
+    for r in ranks:
+        r.begin(frame)
+    r0 = ranks[0]
+    for l in reversed(range(r0.levels)):
+        for r in ranks:
+            r.level_begin(l)
+        for it in range(r0.gn[l]):
+            for r in ranks:
+                r.linearize(l, it)
+            for s in range(r0.patch_iters):
+                for r in ranks:
+                    r.sweep(l, s)
+                if s < r0.patch_iters - 1:
+                    comm.halo(ranks, l, r0.lib.hwf_split_swept(s).decode())
+            comm.allgather_rows(ranks, l, "total")
+            comm.allgather_rows(ranks, l, "delta")
+        for r in ranks:
+            r.energy_after(l)
+        for r in ranks:
+            r.level_end(l)
+    comm.allreduce_sum(ranks, "energy")
+    comm.allreduce_or(ranks, "flags")
+    out = [r.finish() for r in ranks]
+    del keep
+    return out

@@ -33,18 +33,19 @@ def cuda_lib():
 
 
 def test_cuda_library_exports_every_declared_symbol(cuda_lib):
-    decl = declared("hwflow_c.h") | declared("hwflow_ext.h")
+    decl = declared("hwflow_c.h") | declared("hwflow_ext.h") | declared("hwflow_split.h")
     assert decl, "no declarations parsed"
     assert decl <= exported(cuda_lib), decl - exported(cuda_lib)
     assert set(capi.EXPORTED) == declared("hwflow_c.h")
     assert set(capi.EXPORTED_EXT) == declared("hwflow_ext.h")
+    assert set(capi.EXPORTED_SPLIT) == declared("hwflow_split.h")
 
 
 def test_oracle_libraries_export_the_reference_boundary():
     build.build_oracle()
     for lib in (build.ORACLE_LIB, build.REF_LIB):
         if lib.exists():
-            assert declared("hwflow_c.h") <= exported(lib)
+            assert declared("hwflow_c.h") | declared("hwflow_split.h") <= exported(lib)
 
 
 def test_cuda_library_is_sm100a(cuda_lib):
