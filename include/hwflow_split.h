@@ -15,7 +15,7 @@
  *     neighbours' previous values, so this halo exchange is exact.
  *   - After every Gauss-Newton iteration: all-gather the owned rows of total and delta.
  *   - After the last level: sum the energy partials (all-reduce) and OR the flags.
- * The result is bitwise identical to hwf_solve_pair (flows, visibility). Energies
+ * Flows and visibility are bitwise identical to the unsplit hwf_solve_pair result. Energies
  * agree to rounding, because the node-energy partials of a boundary CTA are
  * summed per rank.
  *
