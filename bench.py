@@ -51,19 +51,29 @@ def workload_desc(mode: str) -> str:
 def extra_configs(dev, lib, h, C, capi, reps: int = 5) -> dict:
     """The other BASELINE.json shapes on this GPU, device-resident replays (not the headline):
     cfg3 1920x1080 occluder + illumination change, 5 levels, 8 px grid, batch 4;
-    cfg5 3840x2160 single frame pair, 5 levels, 4 px grid (north_star: >= 30 Hz)."""
+    cfg5 3840x2160 single frame pair, 5 levels, 4 px grid (north_star: >= 30 Hz);
+    SURVEY §8f rank 3 at cfg2 scale, batch 32: stereo-only (active_fields = s, global PCG; the
+    reference's Schwarz mode hits pAp <= 0 on it) and the stereo-hq preset with the epipolar term on
+    (w_epi = 0.5, rectified-rig F)."""
     from paper_1610_07159_b200 import synthetic
     from paper_1610_07159_b200.hwflow import EnergyParams, SolveSchedule
     out = {}
+    F_rect = np.array([[0.0, 0.0, 0.0], [0.0, 0.0, -1.0], [0.0, 1.0, 0.0]])  # x_0^T F x_1 = y_1 - y_0
     cases = [("cfg3_1920x1080_batch4", lambda: np.stack([synthetic.valgaerts_pair(i)[0] for i in range(4)]),
-              SolveSchedule(levels=5, grid_step=8, pcg_iters=5, patch_iters=5)),
+              SolveSchedule(levels=5, grid_step=8, pcg_iters=5, patch_iters=5), EnergyParams(), None),
              ("cfg5_3840x2160_single_frame", lambda: synthetic.uhd_pair(0)[0][None],
-              SolveSchedule(levels=5, grid_step=4, pcg_iters=5, patch_iters=5))]
-    for name, frames_fn, sched in cases:
+              SolveSchedule(levels=5, grid_step=4, pcg_iters=5, patch_iters=5), EnergyParams(), None),
+             ("cfg2_stereo_only_global_pcg_batch32", lambda: make_frames(32, 0),
+              SolveSchedule(levels=4, grid_step=8, pcg_iters=5, subdomain_px=0, active_fields=1), EnergyParams(),
+              None),
+             ("cfg2_stereo_hq_epipolar_batch32", lambda: make_frames(32, 0),
+              SolveSchedule(levels=4, grid_step=8, pcg_iters=5, patch_iters=5), EnergyParams.preset("stereo-hq"),
+              F_rect)]
+    for name, frames_fn, sched, params, F in cases:
         frames = frames_fn()
         n = frames.shape[0]
         try:
-            dev.solve_batch(frames, EnergyParams(), sched, outputs=("grid_total",))
+            dev.solve_batch(frames, params, sched, F, outputs=("grid_total",))
             status = "ok"
         except capi.SolverDivergence:
             status = "diverged-flag"
@@ -358,7 +368,7 @@ def run_ours(args, ws, rank, local):
             "hbm_gbs": achieved,  # dominant kernel, algorithmic bytes / CUDA-event time
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"] if pk["hbm_gbs"] else None, "traffic": traffic,
-                         "kernel": "k_pixel<LIN> (fused data term + cell reduction), finest level",
+                         "kernel": "k_pixel<LIN,U8> (fused data term + cell reduction), finest level, u8 frames sampled directly",
                          "peak_src": pk["src"], "algorithmic_bytes_per_launch": big, "ms_per_launch": l0_ms,
                          "launches_per_step": nk, "share_of_step": pk_ms / ms_per_step if ms_per_step else None},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": B * 4 * N,

@@ -230,6 +230,23 @@ def test_solve_epipolar_and_stereo_only(device, oracle):
     assert np.abs(r.grid_total[:, 2:]).max() == 0.0  # m, d pinned (solver.cpp:218-220)
 
 
+@pytest.mark.parametrize("mode", ["stereo_only", "stereo_hq_epipolar"])
+def test_cfg2_scale_stereo_modes(device, oracle, mode):
+    """SURVEY §8f rank 3 at cfg2 scale (640x480, 4 levels, 8 px grid): stereo-only (active_fields = s,
+    solver.cpp:27-31, 213-226; global PCG) and the stereo-hq preset with the epipolar term (w_epi = 0.5 > 0,
+    energy.cpp:168-192; Schwarz mode) against the oracle."""
+    imgs = synthetic.webcam_pair(5)[0]
+    F = np.array([[0, 0, 0], [0, 0, -1], [0, 1, 0.0]])
+    if mode == "stereo_only":  # global PCG: the reference's Schwarz mode hits pAp <= 0 here (oracle too)
+        S = SolveSchedule(levels=4, grid_step=8, gn_per_level=[1, 1, 2, 2], pcg_iters=5, subdomain_px=0,
+                          active_fields=1)
+        r, _ = _check_solve(device, oracle, imgs, EnergyParams(), S)
+        assert np.abs(r.grid_total[:, 2:]).max() == 0.0
+    else:
+        S = SolveSchedule(levels=4, grid_step=8, gn_per_level=[1, 1, 2, 2], pcg_iters=5, patch_iters=5)
+        _check_solve(device, oracle, imgs, EnergyParams.preset("stereo-hq"), S, F)
+
+
 def test_batch_is_bitwise_independent(device):
     frames = np.stack([synthetic.webcam_pair(i, 128, 96)[0] for i in range(3)])
     S = SolveSchedule(levels=3, grid_step=8, pcg_iters=5, patch_iters=5)
