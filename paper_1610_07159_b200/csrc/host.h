@@ -632,8 +632,10 @@ inline void check_params(const hwf_energy_params* P, const hwf_schedule* S, cons
   if (hwf_validate_params(P) != HWF_OK) throw InvalidArg("energy weights must be >= 0 and eps_huber > 0");
   if (P->w_epi > 0.0 && !F) throw InvalidArg("epipolar term enabled without a fundamental matrix");
   if (S->grid_step < 1 || S->grid_step > 32) throw InvalidArg("grid_step must be in [1, 32] on the device");
-  if (S->subdomain_px > 0 && (S->subdomain_px + S->grid_step - 1) / S->grid_step > 5)
-    throw InvalidArg("subdomain tile must hold <= 5x5 nodes on the device");
+  if (S->subdomain_px > 0) {  // one CTA of <= 1024 threads per subdomain, a thread per unknown
+    const long long side = (static_cast<long long>(S->subdomain_px) + S->grid_step - 1) / S->grid_step;
+    if (6 * side * side > 1024) throw InvalidArg("subdomain tile must hold <= 13x13 nodes on the device");
+  }
   if (S->pcg_iters < 0 || S->patch_iters < 0) throw InvalidArg("negative iteration count");
 }
 

@@ -35,7 +35,9 @@ def image_index(cam: int, time: int) -> int:  # core.hpp:27
     return cam + 2 * time
 
 
-def grid_dims(w: int, h: int, step: int) -> tuple[int, int]:  # warp_grid.cpp:11-14
+def grid_dims(w: int, h: int, step: int) -> tuple[int, int]:  # warp_grid.cpp:8-14
+    if w < 1 or h < 1 or step < 1:
+        raise capi.InvalidArgument(capi.HWF_EINVAL, "WarpGrid: bad dimensions or step")
     return max((w - 1 + step - 1) // step + 1, 2), max((h - 1 + step - 1) // step + 1, 2)
 
 
