@@ -84,9 +84,11 @@ __global__ void k_occ_project(int w, int h, int gw, int gh, int step, const doub
   bad[pair * N + pix] = ok ? 0 : 1;
 }
 
+// Vertices in 1/256 px fixed point, |coordinate| < 2^30 (k_occ_project), so every box
+// extent is exact as a 32-bit unsigned difference.
 struct Tri {
-  long long X[3], Y[3];
-  long long mnx, mxx, mny, mxy;
+  int X[3], Y[3];
+  int mnx, mxx, mny, mxy;
 };
 
 // Vertices of triangle `tri` of the halfway lattice in view e (pin C.2).
@@ -118,20 +120,20 @@ struct RowEdges {
   int E[3], step[3];
   bool tl[3];
 };
-__device__ __forceinline__ void raster_row_tests(const Tri& T, long long yy, long long x0, long long x1, int w,
+__device__ __forceinline__ void raster_row_tests(const Tri& T, int yy, int x0, int x1, int w,
                                                  unsigned long long* zb, unsigned long long key) {
   RowEdges R;
-  const long long Px0 = x0 * 256, Py = yy * 256;
+  const int Px0 = x0 * 256, Py = yy * 256;
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     const int j = (i + 1) % 3;
-    const int dx = static_cast<int>(T.X[j] - T.X[i]), dy = static_cast<int>(T.Y[j] - T.Y[i]);
-    R.E[i] = dx * static_cast<int>(Py - T.Y[i]) - dy * static_cast<int>(Px0 - T.X[i]);
+    const int dx = T.X[j] - T.X[i], dy = T.Y[j] - T.Y[i];
+    R.E[i] = dx * (Py - T.Y[i]) - dy * (Px0 - T.X[i]);
     R.step[i] = -256 * dy;
     R.tl[i] = dy > 0 || (dy == 0 && dx < 0);
   }
-  unsigned long long* row = zb + yy * w;
-  for (long long xx = x0; xx <= x1; ++xx) {
+  unsigned long long* row = zb + static_cast<size_t>(yy) * w;
+  for (int xx = x0; xx <= x1; ++xx) {
     bool in = true;
 #pragma unroll
     for (int i = 0; i < 3; ++i) in = in && (R.E[i] > 0 || (R.E[i] == 0 && R.tl[i]));
@@ -151,15 +153,15 @@ __device__ __forceinline__ int floordiv32(int a, int b) {  // b > 0
   if ((a % b != 0) && (a < 0)) --q;
   return q;
 }
-__device__ __forceinline__ void raster_row_span(const Tri& T, long long yy, long long x0, long long x1, int w,
+__device__ __forceinline__ void raster_row_span(const Tri& T, int yy, int x0, int x1, int w,
                                                 unsigned long long* zb, unsigned long long key) {
-  int lo = 0, hi = static_cast<int>(x1 - x0);
-  const long long Px0 = x0 * 256, Py = yy * 256;
+  int lo = 0, hi = x1 - x0;
+  const int Px0 = x0 * 256, Py = yy * 256;
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     const int j = (i + 1) % 3;
-    const int dx = static_cast<int>(T.X[j] - T.X[i]), dy = static_cast<int>(T.Y[j] - T.Y[i]);
-    const int A = dx * static_cast<int>(Py - T.Y[i]) + dy * static_cast<int>(T.X[i] - Px0);
+    const int dx = T.X[j] - T.X[i], dy = T.Y[j] - T.Y[i];
+    const int A = dx * (Py - T.Y[i]) + dy * (T.X[i] - Px0);
     if (dy > 0) {
       hi = min(hi, floordiv32(A, 256 * dy));
     } else if (dy < 0) {
@@ -168,7 +170,7 @@ __device__ __forceinline__ void raster_row_span(const Tri& T, long long yy, long
       hi = lo - 1;
     }
   }
-  unsigned long long* row = zb + yy * w + x0;
+  unsigned long long* row = zb + static_cast<size_t>(yy) * w + x0;
   for (int k = lo; k <= hi; ++k) atomicMin(row + k, key);
 }
 
@@ -179,18 +181,21 @@ constexpr int kSmallBoxPx = 16;  // triangles whose pixel box exceeds this go to
 __device__ __forceinline__ bool raster_tri(int w, int h, const Tri& T, bool any_bad, float zf, unsigned int tri,
                                            unsigned long long* zb, unsigned long long* queue,
                                            unsigned int* qcount, unsigned long long qtag) {
-  const long long area = (T.X[1] - T.X[0]) * (T.Y[2] - T.Y[0]) - (T.Y[1] - T.Y[0]) * (T.X[2] - T.X[0]);
-  const bool deg = any_bad || area <= 0 || (T.mxx - T.mnx) > kZbufSpanPx * 256 || (T.mxy - T.mny) > kZbufSpanPx * 256;
-  if (deg) return true;
-  const long long x0 = max(0LL, -((-T.mnx) >> 8)), x1 = min(static_cast<long long>(w - 1), T.mxx >> 8);
-  const long long y0 = max(0LL, -((-T.mny) >> 8)), y1 = min(static_cast<long long>(h - 1), T.mxy >> 8);
+  constexpr unsigned kSpan = kZbufSpanPx * 256;
+  if (any_bad || static_cast<unsigned>(T.mxx - T.mnx) > kSpan || static_cast<unsigned>(T.mxy - T.mny) > kSpan)
+    return true;
+  // within an 8 px box every difference is <= 2^11, so the cross product is exact in int32
+  const int area = (T.X[1] - T.X[0]) * (T.Y[2] - T.Y[0]) - (T.Y[1] - T.Y[0]) * (T.X[2] - T.X[0]);
+  if (area <= 0) return true;
+  const int x0 = max(0, -((-T.mnx) >> 8)), x1 = min(w - 1, T.mxx >> 8);
+  const int y0 = max(0, -((-T.mny) >> 8)), y1 = min(h - 1, T.mxy >> 8);
   if (x1 < x0 || y1 < y0) return false;
   if ((x1 - x0 + 1) * (y1 - y0 + 1) > kSmallBoxPx) {
     queue[atomicAdd(qcount, 1u)] = qtag | tri;
     return false;
   }
   const unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(zf)) << 32) | tri;
-  for (long long yy = y0; yy <= y1; ++yy) raster_row_tests(T, yy, x0, x1, w, zb, key);
+  for (int yy = y0; yy <= y1; ++yy) raster_row_tests(T, yy, x0, x1, w, zb, key);
   return false;
 }
 
@@ -244,10 +249,10 @@ __global__ void k_occ_raster_big(int w, int h, const int2* __restrict__ q, const
     const float zf = fminf(ZZ[v0], fminf(ZZ[v1], ZZ[v2]));
     const unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(zf)) << 32) |
                                    static_cast<unsigned int>(tri);
-    const long long x0 = max(0LL, -((-T.mnx) >> 8)), x1 = min(static_cast<long long>(w - 1), T.mxx >> 8);
-    const long long y0 = max(0LL, -((-T.mny) >> 8)), y1 = min(static_cast<long long>(h - 1), T.mxy >> 8);
+    const int x0 = max(0, -((-T.mnx) >> 8)), x1 = min(w - 1, T.mxx >> 8);
+    const int y0 = max(0, -((-T.mny) >> 8)), y1 = min(h - 1, T.mxy >> 8);
     unsigned long long* zb = zbuf + (static_cast<size_t>(pair) * 4 + e) * N;
-    for (long long yy = y0 + lane; yy <= y1; yy += 32) raster_row_span(T, yy, x0, x1, w, zb, key);
+    for (int yy = y0 + lane; yy <= y1; yy += 32) raster_row_span(T, yy, x0, x1, w, zb, key);
   }
 }
 
