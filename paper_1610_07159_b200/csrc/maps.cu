@@ -228,15 +228,20 @@ __global__ void k_occ_raster(int w, int h, const int2* __restrict__ q, const flo
   raster_tri(w, h, T, b10 || b11 || b01, fminf(z10, fminf(z11, z01)), tri0 + 1, zb, queue, qcount, qtag);
 }
 
-// Warp per queued large triangle; one lane per pixel row of its box.
+// Thread per (queued large triangle, pixel row of its box): boxes are at most
+// kZbufSpanPx + 1 rows tall (larger ones are degenerate), so a triangle's rows
+// are consecutive work items.
 __global__ void k_occ_raster_big(int w, int h, const int2* __restrict__ q, const float* __restrict__ Z,
                                  unsigned long long* __restrict__ zbuf, const unsigned long long* __restrict__ queue,
                                  const unsigned int* __restrict__ qcount) {
-  const int lane = threadIdx.x & 31;
-  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarp = (gridDim.x * blockDim.x) >> 5;
+  constexpr int kRows = kZbufSpanPx + 1;
   const unsigned int n = *qcount;
   const size_t N = static_cast<size_t>(w) * h;
-  for (unsigned int i = gwarp; i < n; i += nwarp) {
+  const unsigned long long items = static_cast<unsigned long long>(n) * kRows;
+  for (unsigned long long it = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x; it < items;
+       it += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+    const unsigned int i = static_cast<unsigned int>(it / kRows);
+    const int row = static_cast<int>(it % kRows);
     const unsigned long long item = queue[i];
     const int pair = static_cast<int>(item >> 34), e = static_cast<int>((item >> 32) & 3);
     const long long tri = static_cast<long long>(item & 0xffffffffULL);
@@ -252,7 +257,7 @@ __global__ void k_occ_raster_big(int w, int h, const int2* __restrict__ q, const
     const int x0 = max(0, -((-T.mnx) >> 8)), x1 = min(w - 1, T.mxx >> 8);
     const int y0 = max(0, -((-T.mny) >> 8)), y1 = min(h - 1, T.mxy >> 8);
     unsigned long long* zb = zbuf + (static_cast<size_t>(pair) * 4 + e) * N;
-    for (int yy = y0 + lane; yy <= y1; yy += 32) raster_row_span(T, yy, x0, x1, w, zb, key);
+    if (y0 + row <= y1) raster_row_span(T, y0 + row, x0, x1, w, zb, key);
   }
 }
 
