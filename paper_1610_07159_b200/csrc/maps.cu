@@ -207,25 +207,31 @@ __global__ void k_occ_raster(int w, int h, const int2* __restrict__ q, const flo
                              uint8_t* __restrict__ degen, unsigned long long* __restrict__ queue,
                              unsigned int* __restrict__ qcount) {
   const int cw = w - 1;
-  const int cx = blockIdx.x * blockDim.x + threadIdx.x, cy = blockIdx.y / 4, e = blockIdx.y % 4, pair = blockIdx.z;
+  const int cx = blockIdx.x * blockDim.x + threadIdx.x, cy = blockIdx.y, pair = blockIdx.z;
   if (cx >= cw) return;
   const size_t N = static_cast<size_t>(w) * h;
   const int i00 = cy * w + cx, i10 = i00 + 1, i01 = i00 + w, i11 = i01 + 1;
-  const int2* Q = q + (static_cast<size_t>(pair) * 4 + e) * N;
   const uint8_t* B = bad + pair * N;
   const float* ZZ = Z + pair * N;
-  const int2 p00 = Q[i00], p10 = Q[i10], p01 = Q[i01], p11 = Q[i11];
   const bool b00 = B[i00], b10 = B[i10], b01 = B[i01], b11 = B[i11];
   const float z00 = ZZ[i00], z10 = ZZ[i10], z01 = ZZ[i01], z11 = ZZ[i11];
-  unsigned long long* zb = zbuf + (static_cast<size_t>(pair) * 4 + e) * N;
-  const unsigned long long qtag = (static_cast<unsigned long long>(pair) << 34) | (static_cast<unsigned long long>(e) << 32);
+  const bool bad0 = b00 || b10 || b01, bad1 = b10 || b11 || b01;
+  const float zf0 = fminf(z00, fminf(z10, z01)), zf1 = fminf(z10, fminf(z11, z01));  // flat depth per triangle
   const unsigned int tri0 = static_cast<unsigned int>(2 * (cy * cw + cx));
-  Tri T;
-  make_tri(p00, p10, p01, T);
-  const bool d0 = raster_tri(w, h, T, b00 || b10 || b01, fminf(z00, fminf(z10, z01)), tri0, zb, queue, qcount, qtag);
-  degen[(static_cast<size_t>(pair) * 4 + e) * N + i00] = d0 ? 1 : 0;
-  make_tri(p10, p11, p01, T);
-  raster_tri(w, h, T, b10 || b11 || b01, fminf(z10, fminf(z11, z01)), tri0 + 1, zb, queue, qcount, qtag);
+#pragma unroll 1
+  for (int e = 0; e < 4; ++e) {  // the 4 views share the cell's depth and validity
+    const int2* Q = q + (static_cast<size_t>(pair) * 4 + e) * N;
+    const int2 p00 = Q[i00], p10 = Q[i10], p01 = Q[i01], p11 = Q[i11];
+    unsigned long long* zb = zbuf + (static_cast<size_t>(pair) * 4 + e) * N;
+    const unsigned long long qtag =
+        (static_cast<unsigned long long>(pair) << 34) | (static_cast<unsigned long long>(e) << 32);
+    Tri T;
+    make_tri(p00, p10, p01, T);
+    const bool d0 = raster_tri(w, h, T, bad0, zf0, tri0, zb, queue, qcount, qtag);
+    degen[(static_cast<size_t>(pair) * 4 + e) * N + i00] = d0 ? 1 : 0;
+    make_tri(p10, p11, p01, T);
+    raster_tri(w, h, T, bad1, zf1, tri0 + 1, zb, queue, qcount, qtag);
+  }
 }
 
 // Thread per (queued large triangle, pixel row of its box): boxes are at most
@@ -504,7 +510,7 @@ void launch_occlusion(int w, int h, int gw, int gh, int step, const double* tota
   if (w >= 2 && h >= 2) {
     cudaMemsetAsync(zbuf, 0xFF, N * 4 * B * sizeof(unsigned long long), s);
     cudaMemsetAsync(qcount, 0, sizeof(unsigned int), s);
-    k_occ_raster<<<dim3((w - 1 + kThreads - 1) / kThreads, 4 * (h - 1), B), kThreads, 0, s>>>(
+    k_occ_raster<<<dim3((w - 1 + kThreads - 1) / kThreads, h - 1, B), kThreads, 0, s>>>(
         w, h, q, Z, bad, zbuf, degen, queue, qcount);
     k_occ_raster_big<<<148 * 8, kThreads, 0, s>>>(w, h, q, Z, zbuf, queue, qcount);
   }
