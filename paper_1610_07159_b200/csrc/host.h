@@ -75,6 +75,8 @@ struct LevelDev {
   double *img = nullptr, *illum = nullptr, *base = nullptr, *delta = nullptr, *total = nullptr;
   double *nodew = nullptr, *nodew2 = nullptr, *nodew_a = nullptr, *nodew_b = nullptr, *half = nullptr, *cells = nullptr, *sys = nullptr, *xa = nullptr, *xb = nullptr,
          *hm = nullptr;
+  const double* hmc = nullptr;  // the coarser level's half maps (illumination of this level), or null
+  int wc = 0, hc = 0;           // their dims
   uint8_t *vis = nullptr, *W = nullptr, *occ = nullptr;
   int n_pix_cta = 0, n_node_cta = 0;
 
@@ -172,8 +174,8 @@ struct Launches {
 // input read once, every output written once.
 inline double pixel_bytes(const LevelDev& d, int B, bool illum, bool u8) {
   // 4 images ({v, gx} + gy sample planes, or the u8 frames at the finest level),
-  // illumination, vis4 + W in/out, halfway out
-  const double perpix = 4 * (u8 ? 1.0 : 24.0) + (illum ? 4 * 8.0 : 0.0) + 1 + 1 + 1 + 8;
+  // illumination (2 coarse half maps, one value per 2x2 pixels), vis4 + W in/out, halfway out
+  const double perpix = 4 * (u8 ? 1.0 : 24.0) + (illum ? 2 * 8.0 / 4.0 : 0.0) + 1 + 1 + 1 + 8;
   return B * (d.N * perpix + d.G * 48.0 + d.C * kCellStride * 8.0);
 }
 
@@ -192,6 +194,7 @@ inline PixArgs pixel_args(const LevelDev& d, const hwf_energy_params& P, const h
   pa.w = d.w; pa.h = d.h; pa.gw = d.gw; pa.gh = d.gh; pa.step = d.step; pa.ncx = d.ncx; pa.ncy = d.ncy;
   pa.tcx = d.tcx; pa.tcy = d.tcy; pa.rp = d.rp;
   pa.pk = d.pk; pa.gy = d.gy; pa.src8 = src8; pa.illum = d.illum; pa.vis4 = d.vis; pa.W = d.W;
+  pa.hmc = d.hmc; pa.wc = d.wc; pa.hc = d.hc;
   pa.total = d.total; pa.half = d.half; pa.cells = d.cells; pa.ep_pair = E.pair_stride(); pa.flags = flags;
   pa.P = to_params(P); pa.active = S.active_fields;
   if (R && !R->whole) {
@@ -227,7 +230,7 @@ inline void rec_linearize(LevelDev& d, int B, const hwf_energy_params& P, const 
   launch_pixel(true, pa, B, st);
   if (L.ev) {
     CK(cudaEventRecordWithFlags((*L.ev)[2 * L.bytes->size() + 1], st, cudaEventRecordExternal));
-    L.bytes->push_back(pixel_bytes(d, B, d.illum != nullptr, src8 != nullptr));
+    L.bytes->push_back(pixel_bytes(d, B, d.hmc != nullptr, src8 != nullptr));
   }
   const bool whole = !R || R->whole;
   launch_structw(d.w, d.h, d.gw, d.gh, d.step, d.half, wnew, B, st, whole ? 0 : R->sw_lo, whole ? -1 : R->sw_hi);
@@ -449,19 +452,24 @@ struct Plan {
     in = alloc_input(N0);
     for (int l = 0; l < L; ++l) {
       LevelDev& d = lv[l];
-      d.img = mem.alloc<double>(B * 4 * d.N);
       if (!u8_finest(l)) {
+        d.img = mem.alloc<double>(B * 4 * d.N);
         d.pk = mem.alloc<double2>(B * 4 * d.N);
         d.gy = mem.alloc<double>(B * 4 * d.N);
       }
       d.alloc_solver(mem, B, S.subdomain_px > 0);
       d.occ = mem.alloc<uint8_t>(B * d.N);
-      if (l < L - 1) d.illum = mem.alloc<double>(B * 4 * d.N);
+
       if (has_prev) {
         prev_delta[l] = mem.alloc<double>(B * d.G * 6);
         prev_total[l] = mem.alloc<double>(B * d.G * 6);
       }
       if (l > 0) d.hm = mem.alloc<double>(B * 2 * d.N);
+      if (l > 0) {  // level l-1 reads this level's half maps as its illumination (pin C.4)
+        lv[l - 1].hmc = d.hm;
+        lv[l - 1].wc = d.w;
+        lv[l - 1].hc = d.h;
+      }
     }
     sc.alloc(mem, B, N0, lv[0].G, true, L > 1, S.subdomain_px <= 0);
     E.nslots = std::max(nslots, 1);
@@ -508,11 +516,16 @@ struct Plan {
   void rec_prologue(cudaStream_t st, Launches& LC) {
     CK(cudaMemsetAsync(E.part, 0, sizeof(double) * B * E.pair_stride(), st));
     CK(cudaMemsetAsync(flags, 0, sizeof(int) * B, st));
-    // pyramid (image.cpp:177-185)
-    launch_pyr_in(in, dtype, lv[0].img, static_cast<long long>(B) * 4 * lv[0].N, st);
-    LC.count++;
+    // pyramid (image.cpp:177-185); u8 frames: level 1 comes from the bytes, level 0 is never stored
+    if (!u8_finest(0)) {
+      launch_pyr_in(in, dtype, lv[0].img, static_cast<long long>(B) * 4 * lv[0].N, st);
+      LC.count++;
+    }
     for (int l = 1; l < L; ++l) {
-      launch_pyr_down(lv[l - 1].img, lv[l - 1].w, lv[l - 1].h, lv[l].img, lv[l].w, lv[l].h, 4 * B, st);
+      if (l == 1 && u8_finest(0))
+        launch_pyr_down_u8(static_cast<const uint8_t*>(in), lv[0].w, lv[0].h, lv[1].img, lv[1].w, lv[1].h, 4 * B, st);
+      else
+        launch_pyr_down(lv[l - 1].img, lv[l - 1].w, lv[l - 1].h, lv[l].img, lv[l].w, lv[l].h, 4 * B, st);
       LC.count++;
     }
     for (int l = 0; l < L; ++l) {
@@ -533,7 +546,7 @@ struct Plan {
     } else {  // prolongation
       const LevelDev& c = lv[l + 1];
       launch_prolong_grid(c.gw, c.gh, d.gw, d.gh, d.step, c.total, d.base, d.total, d.delta, B, st);
-      launch_prolong_maps(c.w, c.h, d.w, d.h, c.occ, c.hm, d.vis, d.illum, B, st);
+      launch_prolong_maps(c.w, c.h, d.w, d.h, c.occ, nullptr, d.vis, nullptr, B, st);
       LC.count += 2;
     }
     if (has_prev) {  // warm start: delta_l = advected previous delta

@@ -22,7 +22,11 @@ struct PixArgs {
   const double2* pk;    // [B][4][N] {value, grad x} (k_pack)
   const double* gy;     // [B][4][N] grad y (k_pack)
   const uint8_t* src8;  // [B][4][N] u8 frames of the finest level (then pk/gy unused), or null
-  const double* illum;  // [B][4][N] or null
+  const double* illum;  // [B][4][N] or null (stage seams: explicit maps)
+  // pipeline: the coarser level's half maps [B][2][wc*hc]; illum of image e at (x, y) is
+  // (e odd ? -1 : +1) * hmc[e/2][min(y/2, hc-1)][min(x/2, wc-1)] (box upsample, pin C.4)
+  const double* hmc;
+  int wc, hc;
   const uint8_t* vis4;  // [B][N]
   uint8_t* W;           // [B][N] in: current bits; out: refreshed bits (refresh)
   const double* total;  // [B][G][6]
@@ -117,6 +121,7 @@ void launch_pcg_global(const PcgArgs& a, int B, cudaStream_t s);
 
 // maps.cu
 void launch_pyr_in(const void* src, int dtype, double* dst, long long n, cudaStream_t s);
+void launch_pyr_down_u8(const uint8_t* src, int w, int h, double* dst, int ow, int oh, int planes, cudaStream_t s);
 void launch_pyr_down(const double* src, int w, int h, double* dst, int ow, int oh, int planes,
                      cudaStream_t s);
 void launch_init_coarse(double* base, double* total, double* delta, int G, int B, double ox,

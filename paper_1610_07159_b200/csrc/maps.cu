@@ -27,6 +27,27 @@ __global__ void k_pyr_in(const void* __restrict__ src, int dtype, double* __rest
   }
 }
 
+// Level 1 straight from u8 frames: the level-0 values k/255 (k_pyr_in) are rebuilt in
+// registers and averaged exactly as k_pyr_down does, so level 0 is never materialised.
+__global__ void k_pyr_down_u8(const uint8_t* __restrict__ src, int w, int h, double* __restrict__ dst, int ow,
+                              int oh) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+  const int plane = blockIdx.z;
+  if (x >= ow) return;
+  const uint8_t* S = src + static_cast<size_t>(plane) * w * h;
+  double sum = 0.0;
+  int cnt = 0;
+  for (int dy = 0; dy < 2; ++dy)
+    for (int dx = 0; dx < 2; ++dx) {
+      const int sx = 2 * x + dx, sy = 2 * y + dy;
+      if (sx < w && sy < h) {
+        sum = __dadd_rn(sum, __ddiv_rn(static_cast<double>(S[static_cast<size_t>(sy) * w + sx]), 255.0));
+        ++cnt;
+      }
+    }
+  dst[static_cast<size_t>(plane) * ow * oh + static_cast<size_t>(y) * ow + x] = __ddiv_rn(sum, static_cast<double>(cnt));
+}
+
 __global__ void k_pyr_down(const double* __restrict__ src, int w, int h, double* __restrict__ dst,
                            int ow, int oh) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
@@ -493,6 +514,9 @@ void init_maps_constants() {
 }
 void launch_pyr_in(const void* src, int dtype, double* dst, long long n, cudaStream_t s) {
   k_pyr_in<<<static_cast<unsigned>((n + kThreads - 1) / kThreads), kThreads, 0, s>>>(src, dtype, dst, n);
+}
+void launch_pyr_down_u8(const uint8_t* src, int w, int h, double* dst, int ow, int oh, int planes, cudaStream_t s) {
+  k_pyr_down_u8<<<rows_grid(ow, oh, planes), kThreads, 0, s>>>(src, w, h, dst, ow, oh);
 }
 void launch_pyr_down(const double* src, int w, int h, double* dst, int ow, int oh, int planes, cudaStream_t s) {
   k_pyr_down<<<rows_grid(ow, oh, planes), kThreads, 0, s>>>(src, w, h, dst, ow, oh);
