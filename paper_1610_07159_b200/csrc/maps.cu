@@ -41,11 +41,15 @@ __global__ void k_pyr_down_u8(const uint8_t* __restrict__ src, int w, int h, dou
     for (int dx = 0; dx < 2; ++dx) {
       const int sx = 2 * x + dx, sy = 2 * y + dy;
       if (sx < w && sy < h) {
-        sum = __dadd_rn(sum, __ddiv_rn(static_cast<double>(S[static_cast<size_t>(sy) * w + sx]), 255.0));
+        // k/255 correctly rounded as fma(k, hi, k * lo), exhaustively checked (pixel.cu u8val)
+        const double k = static_cast<double>(S[static_cast<size_t>(sy) * w + sx]);
+        sum = __dadd_rn(sum, __fma_rn(k, 1.0 / 255.0, __dmul_rn(k, 5.4633625097902372e-20)));
         ++cnt;
       }
     }
-  dst[static_cast<size_t>(plane) * ow * oh + static_cast<size_t>(y) * ow + x] = __ddiv_rn(sum, static_cast<double>(cnt));
+  // cnt is 1, 2 or 4: dividing by it is an exact scaling
+  dst[static_cast<size_t>(plane) * ow * oh + static_cast<size_t>(y) * ow + x] =
+      __dmul_rn(sum, cnt == 4 ? 0.25 : (cnt == 2 ? 0.5 : 1.0));
 }
 
 __global__ void k_pyr_down(const double* __restrict__ src, int w, int h, double* __restrict__ dst,
@@ -64,7 +68,9 @@ __global__ void k_pyr_down(const double* __restrict__ src, int w, int h, double*
         ++cnt;
       }
     }
-  dst[static_cast<size_t>(plane) * ow * oh + static_cast<size_t>(y) * ow + x] = __ddiv_rn(sum, static_cast<double>(cnt));
+  // sum / cnt (image.cpp:117) with cnt in {1, 2, 4}: an exact power-of-two scaling
+  dst[static_cast<size_t>(plane) * ow * oh + static_cast<size_t>(y) * ow + x] =
+      __dmul_rn(sum, cnt == 4 ? 0.25 : (cnt == 2 ? 0.5 : 1.0));
 }
 
 __global__ void k_init_coarse(double* base, double* total, double* delta, long long n_nodes, double ox, double oy) {
