@@ -292,7 +292,7 @@ inline void rec_energy_after(LevelDev& d, int B, const hwf_energy_params& P, con
 // The nonlinear loop of one level (solver.cpp:484-532) for a batch, whole level.
 inline void record_gn_level(LevelDev& d, int B, const hwf_energy_params& P, const hwf_schedule& S, const double* dF,
                             int gn, const Energies& E, int slot_base, Scratch& sc, int* flags, cudaStream_t st,
-                            Launches& L, const uint8_t* src8 = nullptr) {
+                            Launches& L, const uint8_t* src8 = nullptr, bool energy_after = true) {
   for (int it = 0; it < gn; ++it) {
     rec_linearize(d, B, P, S, dF, it, E, slot_base, flags, st, L, src8);
     if (S.subdomain_px > 0) {
@@ -306,7 +306,7 @@ inline void record_gn_level(LevelDev& d, int B, const hwf_energy_params& P, cons
       L.count += 1;
     }
   }
-  if (gn > 0) rec_energy_after(d, B, P, S, dF, gn, E, slot_base, flags, st, L, src8);
+  if (gn > 0 && energy_after) rec_energy_after(d, B, P, S, dF, gn, E, slot_base, flags, st, L, src8);
 }
 
 // ---- the batched plan (one CUDA graph per configuration) ------------------------
@@ -335,6 +335,8 @@ struct Plan {
   double *o_s = nullptr, *o_m = nullptr, *o_d = nullptr, *o_disp = nullptr;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
+  cudaStream_t side = nullptr;  // capture-time branch for the per-level E_after pass
+  cudaEvent_t fork_ev[HWF_MAX_LEVELS] = {}, join_ev[HWF_MAX_LEVELS] = {};
   // streaming (hwf_submit_batch / hwf_wait): two input/result slots, one graph each
   bool async_ready = false;
   void* in_slot[2] = {};
@@ -360,6 +362,11 @@ struct Plan {
     return !F_ || std::memcmp(F, F_, sizeof(F)) == 0;
   }
   ~Plan() {
+    if (side) cudaStreamDestroy(side);
+    for (int l = 0; l < HWF_MAX_LEVELS; ++l) {
+      if (fork_ev[l]) cudaEventDestroy(fork_ev[l]);
+      if (join_ev[l]) cudaEventDestroy(join_ev[l]);
+    }
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
     if (exec_slot[1]) cudaGraphExecDestroy(exec_slot[1]);
@@ -502,12 +509,26 @@ struct Plan {
       LC.ev = &ev;
       LC.bytes = &ev_bytes;
     }
+    if (!side) {
+      CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+      for (int l = 0; l < L; ++l) {
+        CK(cudaEventCreateWithFlags(&fork_ev[l], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&join_ev[l], cudaEventDisableTiming));
+      }
+    }
     rec_prologue(st, LC);
     for (int l = L - 1; l >= 0; --l) {
       rec_level_begin(l, st, LC);
-      record_gn_level(lv[l], B, P, S, dF, gn[l], E, slot_base[l], sc, flags, st, LC, src8(l));
+      record_gn_level(lv[l], B, P, S, dF, gn[l], E, slot_base[l], sc, flags, st, LC, src8(l), false);
+      // E_after of the level's last iteration only feeds the stats: a graph branch beside the
+      // occlusion and illumination of the same level (which do not touch its inputs)
+      CK(cudaEventRecord(fork_ev[l], st));
+      CK(cudaStreamWaitEvent(side, fork_ev[l], 0));
+      if (gn[l] > 0) rec_energy_after(lv[l], B, P, S, dF, gn[l], E, slot_base[l], flags, side, LC, src8(l));
+      CK(cudaEventRecord(join_ev[l], side));
       rec_level_end(l, st, LC);
     }
+    for (int l = 0; l < L; ++l) CK(cudaStreamWaitEvent(st, join_ev[l], 0));
     rec_epilogue(st, LC);
     launches = LC.count;
   }
