@@ -40,6 +40,7 @@ int hwf_create(int device, hwf_ctx** out) {
     return HWF_ECUDA;
   }
   init_pixel_attributes();
+  init_solve_attributes();
   init_maps_constants();
   if (cudaGetLastError() != cudaSuccess) {
     delete c;

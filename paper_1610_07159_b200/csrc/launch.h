@@ -101,6 +101,7 @@ struct PcgArgs {
 
 // once per device, outside any stream capture
 void init_pixel_attributes();
+void init_solve_attributes();
 void init_maps_constants();
 
 // pixel.cu

@@ -13,6 +13,8 @@
 //
 // k_pcg_global: the subdomain_px = 0 mode (pcg_solve, solver.cpp:365-380), one
 // CTA per frame pair looping over all iterations with block-wide fixed-order dots.
+#include <cstdlib>
+
 #include "launch.h"
 
 namespace hwf {
@@ -192,6 +194,196 @@ __global__ void __launch_bounds__(TEAM == 32 ? 128 : TEAM) k_schwarz(const SwzAr
   }
 }
 
+// ---- k_schwarz22: 2x2-node subdomains (16 px tiles at grid step 8, the BASELINE cfg1-3 case) --------
+// Same sweep as k_schwarz<32, 4>, but the subdomain's neighbourhood is staged in shared memory by
+// bulk asynchronous copies (cp.async.bulk -> mbarrier) instead of ~90 scattered 8 B loads per lane:
+// the system records of node rows b-1..b+1 x columns a-1..a+2 (every block the four rows touch
+// lives there: forward slots in the own records, backward ones in the up/left neighbours') and
+// the published x of rows b-1..b+2 x columns a-1..a+2. Lanes then read their rows from shared memory.
+namespace bulk {
+__device__ __forceinline__ uint32_t saddr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(b)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void copy(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(saddr(dst)), "l"(src), "r"(bytes), "r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t phase) {
+  uint32_t done = 0;
+  do {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(done) : "r"(saddr(b)), "r"(phase) : "memory");
+  } while (!done);
+}
+}  // namespace bulk
+
+struct alignas(16) Swz22Smem {
+  double rec[3][4][kSysStride];  // node rows b-1, b, b+1 x columns a-1 .. a+2
+  double pub[4][4][6];           // published x, rows b-1 .. b+2 x columns a-1 .. a+2
+  double psub[32];
+  uint64_t bar;
+};
+
+__global__ void __launch_bounds__(128) k_schwarz22(const SwzArgs a) {
+  extern __shared__ __align__(16) unsigned char swz_raw[];
+  const int team = threadIdx.x >> 5, u = threadIdx.x & 31;
+  Swz22Smem& sm = reinterpret_cast<Swz22Smem*>(swz_raw)[team];
+  const int pair = blockIdx.y;
+  const int sub = a.sub0 + blockIdx.x * 4 + team;
+  const int G = a.gw * a.gh;
+  const bool sub_ok = sub < a.sub1;  // warp-uniform
+  const int tx = sub_ok ? sub % a.ntx : 0, ty = sub_ok ? sub / a.ntx : 0;
+  const int alo = (tx * a.tile + a.step - 1) / a.step, ahi = min(a.gw - 1, ((tx + 1) * a.tile - 1) / a.step);
+  const int blo = (ty * a.tile + a.step - 1) / a.step, bhi = min(a.gh - 1, ((ty + 1) * a.tile - 1) / a.step);
+  const double* sys = a.sys + static_cast<size_t>(pair) * G * kSysStride;
+  const double* pubg = a.pub ? a.pub + static_cast<size_t>(pair) * G * 6 : nullptr;
+  if (!sub_ok) return;
+
+  // stage the neighbourhood (one elected lane issues the copies)
+  if (u == 0) bulk::mbar_init(&sm.bar);
+  __syncwarp();
+  if (u == 0) {
+    uint32_t bytes = 0;
+    const int c0 = max(alo - 1, 0);
+    for (int ry = 0; ry < 3; ++ry) {
+      const int row = blo - 1 + ry;
+      const int c1 = min(alo + (ry == 2 ? 1 : 2), a.gw - 1);
+      if (row >= 0 && row < a.gh && c1 >= c0) bytes += (c1 - c0 + 1) * kSysStride * 8;
+    }
+    if (pubg)
+      for (int ry = 0; ry < 4; ++ry) {
+        const int row = blo - 1 + ry, c1 = min(alo + 2, a.gw - 1);
+        if (row >= 0 && row < a.gh && c1 >= c0) bytes += (c1 - c0 + 1) * 48;
+      }
+    bulk::mbar_expect(&sm.bar, bytes);
+    for (int ry = 0; ry < 3; ++ry) {
+      const int row = blo - 1 + ry;
+      const int c1 = min(alo + (ry == 2 ? 1 : 2), a.gw - 1);
+      if (row >= 0 && row < a.gh && c1 >= c0)
+        bulk::copy(&sm.rec[ry][c0 - (alo - 1)][0], sys + (static_cast<size_t>(row) * a.gw + c0) * kSysStride,
+                   (c1 - c0 + 1) * kSysStride * 8, &sm.bar);
+    }
+    if (pubg)
+      for (int ry = 0; ry < 4; ++ry) {
+        const int row = blo - 1 + ry, c1 = min(alo + 2, a.gw - 1);
+        if (row >= 0 && row < a.gh && c1 >= c0)
+          bulk::copy(&sm.pub[ry][c0 - (alo - 1)][0], pubg + (static_cast<size_t>(row) * a.gw + c0) * 6,
+                     (c1 - c0 + 1) * 48, &sm.bar);
+      }
+  }
+  const int i = u / 6, r = u - 6 * (u / 6);
+  const int ix = i & 1, iy = i >> 1;
+  const int na = alo + ix, nb = blo + iy;
+  const bool act = u < 24 && na <= ahi && nb <= bhi;
+  const int n = act ? nb * a.gw + na : 0;
+  int ro[6];
+#pragma unroll
+  for (int c = 0; c < 6; ++c) ro[c] = sym6(r, c);
+  bulk::mbar_wait(&sm.bar, 0);
+
+  const double* own = &sm.rec[1 + iy][1 + ix][0];
+  double arow[4][6];
+  double b = 0.0, x = 0.0;
+  if (act) {
+    b = own[kSysRhs + r];
+    if (pubg) x = sm.pub[1 + iy][1 + ix][r];
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {  // dense local row over the tile's nodes
+    const int jx = j & 1, jy = j >> 1;
+    const bool ok = act && alo + jx <= ahi && blo + jy <= bhi;
+    const int s9 = (jy - iy + 1) * 3 + (jx - ix + 1);
+    const double* blk = s9 >= 4 ? own + (s9 - 4) * 21 : &sm.rec[1 + jy][1 + jx][0] + (4 - s9) * 21;
+#pragma unroll
+    for (int c = 0; c < 6; ++c) arow[j][c] = ok ? blk[ro[c]] : 0.0;
+  }
+  if (pubg) {  // coupling to the frozen neighbours (solver.cpp:437-448), two alternating chains
+    double b0 = 0.0, b1 = 0.0;
+#pragma unroll
+    for (int s9 = 0; s9 < 9; ++s9) {
+      if (s9 == 4) continue;
+      const int dx = s9 % 3 - 1, dy = s9 / 3 - 1;
+      const int qa = na + dx, qb = nb + dy;
+      const bool valid = act && qa >= 0 && qa < a.gw && qb >= 0 && qb < a.gh;
+      const bool local = qa >= alo && qa <= ahi && qb >= blo && qb <= bhi;
+      if (!valid || local) continue;
+      const double* blk = s9 >= 4 ? own + (s9 - 4) * 21 : &sm.rec[1 + iy + dy][1 + ix + dx][0] + (4 - s9) * 21;
+      const double* pv = &sm.pub[1 + iy + dy][1 + ix + dx][0];
+#pragma unroll
+      for (int c = 0; c < 6; c += 2) {
+        b0 += blk[ro[c]] * pv[c];
+        b1 += blk[ro[c + 1]] * pv[c + 1];
+      }
+    }
+    b -= b0 + b1;
+  }
+  double m_self = 1.0, m_cross = 0.0;  // solver.cpp:468-474
+  if (act) {
+    const double* pre = own + kSysPre + 3 * (r >> 1);
+    m_self = pre[(r & 1) ? 2 : 0];
+    m_cross = pre[1];
+  }
+  auto apply = [&](double v) {  // local block SpMV (solver.cpp:452-467)
+    __syncwarp();
+    sm.psub[u] = v;
+    __syncwarp();
+    double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int c = 0; c < 6; ++c) acc[c % 3] += arow[j][c] * sm.psub[6 * j + c];
+    return act ? (acc[0] + acc[1]) + acc[2] : 0.0;
+  };
+  auto precond = [&](double rv) {
+    const double partner = __shfl_xor_sync(0xffffffffu, rv, 1);
+    return act ? m_self * rv + m_cross * partner : 0.0;
+  };
+  // pcg_impl (solver.cpp:320-361), warm start x0 = published
+  double res = b - apply(x);
+  double z = precond(res);
+  double rz = warp_sum(res * z);
+  const double rz0 = fabs(rz);
+  int flag = 0;
+  if (rz0 != 0.0) {
+    double p = z;
+    for (int it = 0; it < a.pcg_iters; ++it) {
+      const double ap = apply(p);
+      const double pAp = warp_sum(p * ap);
+      if (pAp <= 0.0) {
+        flag = kFlagCurvature;
+        break;
+      }
+      const double alpha = rz / pAp;
+      x += alpha * p;
+      res -= alpha * ap;
+      z = precond(res);
+      const double rzn = warp_sum(res * z);
+      if (fabs(rzn) > 100.0 * rz0) {
+        flag = kFlagGrowth;
+        break;
+      }
+      const double beta = rzn / rz;
+      rz = rzn;
+      p = z + beta * p;
+    }
+  }
+  if (!act) return;
+  if (flag && u == 0) atomicOr(a.flags + pair, flag);
+  const size_t o = (static_cast<size_t>(pair) * G + n) * 6 + r;
+  if (a.last) {
+    if (!isfinite(x)) atomicOr(a.flags + pair, kFlagStep);
+    if ((a.active >> (r >> 1)) & 1) a.delta[o] += x;
+    a.total[o] = a.base[o] + a.delta[o];
+  } else {
+    a.next[o] = x;
+  }
+}
+
 constexpr int kPcgThreads = 1024;
 
 __device__ double block_dot(const double* __restrict__ x, const double* __restrict__ y, int n, double* red) {
@@ -313,6 +505,10 @@ __global__ void __launch_bounds__(kPcgThreads) k_pcg_global(const PcgArgs a) {
 
 }  // namespace
 
+void init_solve_attributes() {
+  cudaFuncSetAttribute(k_schwarz22, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * sizeof(Swz22Smem));
+}
+
 void launch_schwarz(const SwzArgs& a_in, int B, cudaStream_t s) {
   SwzArgs a = a_in;
   if (a.sub1 <= 0) {  // whole level
@@ -322,7 +518,13 @@ void launch_schwarz(const SwzArgs& a_in, int B, cudaStream_t s) {
   const int nsub = a.sub1 - a.sub0;
   if (nsub <= 0) return;
   const int nodes = a.nxm * a.nym;
-  if (nodes <= 4) {
+  static const bool use22 = [] {
+    const char* e = std::getenv("HWF_SWZ22");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (use22 && a.nxm == 2 && a.nym == 2) {
+    k_schwarz22<<<dim3((nsub + 3) / 4, B), 128, 4 * sizeof(Swz22Smem), s>>>(a);
+  } else if (nodes <= 4) {
     k_schwarz<32, 4><<<dim3((nsub + 3) / 4, B), 128, 0, s>>>(a);
   } else if (6 * nodes <= 128) {
     k_schwarz<128, 0><<<dim3(nsub, B), 128, 0, s>>>(a);
