@@ -13,6 +13,7 @@
 //
 // k_pcg_global: the subdomain_px = 0 mode (pcg_solve, solver.cpp:365-380), one
 // CTA per frame pair looping over all iterations with block-wide fixed-order dots.
+#include <algorithm>
 #include <cstdlib>
 
 #include "launch.h"
@@ -229,158 +230,190 @@ struct alignas(16) Swz22Smem {
   uint64_t bar;
 };
 
-__global__ void __launch_bounds__(128) k_schwarz22(const SwzArgs a) {
+struct Tile22 {  // one subdomain of the launch's range
+  int pair, alo, ahi, blo, bhi;
+};
+__device__ __forceinline__ Tile22 tile22(const SwzArgs& a, int t, int nsub) {
+  Tile22 T;
+  T.pair = t / nsub;
+  const int sub = a.sub0 + (t - T.pair * nsub);
+  const int tx = sub % a.ntx, ty = sub / a.ntx;
+  T.alo = (tx * a.tile + a.step - 1) / a.step;
+  T.ahi = min(a.gw - 1, ((tx + 1) * a.tile - 1) / a.step);
+  T.blo = (ty * a.tile + a.step - 1) / a.step;
+  T.bhi = min(a.gh - 1, ((ty + 1) * a.tile - 1) / a.step);
+  return T;
+}
+
+// Lane 0: arm the barrier with the tile's byte count and issue its bulk copies.
+__device__ __forceinline__ void stage22(const SwzArgs& a, const Tile22& T, Swz22Smem& sm) {
+  const size_t G = static_cast<size_t>(a.gw) * a.gh;
+  const double* sys = a.sys + T.pair * G * kSysStride;
+  const double* pubg = a.pub ? a.pub + T.pair * G * 6 : nullptr;
+  const int c0 = max(T.alo - 1, 0);
+  uint32_t bytes = 0;
+  for (int ry = 0; ry < 3; ++ry) {
+    const int row = T.blo - 1 + ry, c1 = min(T.alo + (ry == 2 ? 1 : 2), a.gw - 1);
+    if (row >= 0 && row < a.gh && c1 >= c0) bytes += (c1 - c0 + 1) * kSysStride * 8;
+  }
+  if (pubg)
+    for (int ry = 0; ry < 4; ++ry) {
+      const int row = T.blo - 1 + ry, c1 = min(T.alo + 2, a.gw - 1);
+      if (row >= 0 && row < a.gh && c1 >= c0) bytes += (c1 - c0 + 1) * 48;
+    }
+  bulk::mbar_expect(&sm.bar, bytes);
+  for (int ry = 0; ry < 3; ++ry) {
+    const int row = T.blo - 1 + ry, c1 = min(T.alo + (ry == 2 ? 1 : 2), a.gw - 1);
+    if (row >= 0 && row < a.gh && c1 >= c0)
+      bulk::copy(&sm.rec[ry][c0 - (T.alo - 1)][0], sys + (static_cast<size_t>(row) * a.gw + c0) * kSysStride,
+                 (c1 - c0 + 1) * kSysStride * 8, &sm.bar);
+  }
+  if (pubg)
+    for (int ry = 0; ry < 4; ++ry) {
+      const int row = T.blo - 1 + ry, c1 = min(T.alo + 2, a.gw - 1);
+      if (row >= 0 && row < a.gh && c1 >= c0)
+        bulk::copy(&sm.pub[ry][c0 - (T.alo - 1)][0], pubg + (static_cast<size_t>(row) * a.gw + c0) * 6,
+                   (c1 - c0 + 1) * 48, &sm.bar);
+    }
+}
+
+// Persistent: each warp walks subdomains t = warp, warp + W, ...; the next subdomain's copies
+// are issued as soon as the current one's rows are in registers, so they land during its PCG.
+__global__ void __launch_bounds__(128) k_schwarz22(const SwzArgs a, int nsub, int total) {
   extern __shared__ __align__(16) unsigned char swz_raw[];
   const int team = threadIdx.x >> 5, u = threadIdx.x & 31;
   Swz22Smem& sm = reinterpret_cast<Swz22Smem*>(swz_raw)[team];
-  const int pair = blockIdx.y;
-  const int sub = a.sub0 + blockIdx.x * 4 + team;
-  const int G = a.gw * a.gh;
-  const bool sub_ok = sub < a.sub1;  // warp-uniform
-  const int tx = sub_ok ? sub % a.ntx : 0, ty = sub_ok ? sub / a.ntx : 0;
-  const int alo = (tx * a.tile + a.step - 1) / a.step, ahi = min(a.gw - 1, ((tx + 1) * a.tile - 1) / a.step);
-  const int blo = (ty * a.tile + a.step - 1) / a.step, bhi = min(a.gh - 1, ((ty + 1) * a.tile - 1) / a.step);
-  const double* sys = a.sys + static_cast<size_t>(pair) * G * kSysStride;
-  const double* pubg = a.pub ? a.pub + static_cast<size_t>(pair) * G * 6 : nullptr;
-  if (!sub_ok) return;
-
-  // stage the neighbourhood (one elected lane issues the copies)
-  if (u == 0) bulk::mbar_init(&sm.bar);
-  __syncwarp();
-  if (u == 0) {
-    uint32_t bytes = 0;
-    const int c0 = max(alo - 1, 0);
-    for (int ry = 0; ry < 3; ++ry) {
-      const int row = blo - 1 + ry;
-      const int c1 = min(alo + (ry == 2 ? 1 : 2), a.gw - 1);
-      if (row >= 0 && row < a.gh && c1 >= c0) bytes += (c1 - c0 + 1) * kSysStride * 8;
-    }
-    if (pubg)
-      for (int ry = 0; ry < 4; ++ry) {
-        const int row = blo - 1 + ry, c1 = min(alo + 2, a.gw - 1);
-        if (row >= 0 && row < a.gh && c1 >= c0) bytes += (c1 - c0 + 1) * 48;
-      }
-    bulk::mbar_expect(&sm.bar, bytes);
-    for (int ry = 0; ry < 3; ++ry) {
-      const int row = blo - 1 + ry;
-      const int c1 = min(alo + (ry == 2 ? 1 : 2), a.gw - 1);
-      if (row >= 0 && row < a.gh && c1 >= c0)
-        bulk::copy(&sm.rec[ry][c0 - (alo - 1)][0], sys + (static_cast<size_t>(row) * a.gw + c0) * kSysStride,
-                   (c1 - c0 + 1) * kSysStride * 8, &sm.bar);
-    }
-    if (pubg)
-      for (int ry = 0; ry < 4; ++ry) {
-        const int row = blo - 1 + ry, c1 = min(alo + 2, a.gw - 1);
-        if (row >= 0 && row < a.gh && c1 >= c0)
-          bulk::copy(&sm.pub[ry][c0 - (alo - 1)][0], pubg + (static_cast<size_t>(row) * a.gw + c0) * 6,
-                     (c1 - c0 + 1) * 48, &sm.bar);
-      }
-  }
+  const int W = gridDim.x * 4;
+  int t = blockIdx.x * 4 + team;
+  if (t >= total) return;
+  const size_t G = static_cast<size_t>(a.gw) * a.gh;
   const int i = u / 6, r = u - 6 * (u / 6);
   const int ix = i & 1, iy = i >> 1;
-  const int na = alo + ix, nb = blo + iy;
-  const bool act = u < 24 && na <= ahi && nb <= bhi;
-  const int n = act ? nb * a.gw + na : 0;
   int ro[6];
 #pragma unroll
   for (int c = 0; c < 6; ++c) ro[c] = sym6(r, c);
-  bulk::mbar_wait(&sm.bar, 0);
+  const bool has_pub = a.pub != nullptr;
 
-  const double* own = &sm.rec[1 + iy][1 + ix][0];
-  double arow[4][6];
-  double b = 0.0, x = 0.0;
-  if (act) {
-    b = own[kSysRhs + r];
-    if (pubg) x = sm.pub[1 + iy][1 + ix][r];
-  }
+  if (u == 0) bulk::mbar_init(&sm.bar);
+  __syncwarp();
+  Tile22 T = tile22(a, t, nsub);
+  if (u == 0) stage22(a, T, sm);
+  uint32_t phase = 0;
+  for (; t < total; t += W) {
+    const int na = T.alo + ix, nb = T.blo + iy;
+    const bool act = u < 24 && na <= T.ahi && nb <= T.bhi;
+    const int n = act ? nb * a.gw + na : 0;
+    const int pair = T.pair;
+    const int alo = T.alo, ahi = T.ahi, blo = T.blo, bhi = T.bhi;
+    bulk::mbar_wait(&sm.bar, phase);
+    phase ^= 1;
+
+    const double* own = &sm.rec[1 + iy][1 + ix][0];
+    double arow[4][6];
+    double b = 0.0, x = 0.0;
+    if (act) {
+      b = own[kSysRhs + r];
+      if (has_pub) x = sm.pub[1 + iy][1 + ix][r];
+    }
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {  // dense local row over the tile's nodes
-    const int jx = j & 1, jy = j >> 1;
-    const bool ok = act && alo + jx <= ahi && blo + jy <= bhi;
-    const int s9 = (jy - iy + 1) * 3 + (jx - ix + 1);
-    const double* blk = s9 >= 4 ? own + (s9 - 4) * 21 : &sm.rec[1 + jy][1 + jx][0] + (4 - s9) * 21;
+    for (int j = 0; j < 4; ++j) {  // dense local row over the tile's nodes
+      const int jx = j & 1, jy = j >> 1;
+      const bool ok = act && alo + jx <= ahi && blo + jy <= bhi;
+      const int s9 = (jy - iy + 1) * 3 + (jx - ix + 1);
+      const double* blk = s9 >= 4 ? own + (s9 - 4) * 21 : &sm.rec[1 + jy][1 + jx][0] + (4 - s9) * 21;
 #pragma unroll
-    for (int c = 0; c < 6; ++c) arow[j][c] = ok ? blk[ro[c]] : 0.0;
-  }
-  if (pubg) {  // coupling to the frozen neighbours (solver.cpp:437-448), two alternating chains
-    double b0 = 0.0, b1 = 0.0;
+      for (int c = 0; c < 6; ++c) arow[j][c] = ok ? blk[ro[c]] : 0.0;
+    }
+    if (has_pub) {  // coupling to the frozen neighbours (solver.cpp:437-448), two alternating chains
+      double b0 = 0.0, b1 = 0.0;
 #pragma unroll
-    for (int s9 = 0; s9 < 9; ++s9) {
-      if (s9 == 4) continue;
-      const int dx = s9 % 3 - 1, dy = s9 / 3 - 1;
-      const int qa = na + dx, qb = nb + dy;
-      const bool valid = act && qa >= 0 && qa < a.gw && qb >= 0 && qb < a.gh;
-      const bool local = qa >= alo && qa <= ahi && qb >= blo && qb <= bhi;
-      if (!valid || local) continue;
-      const double* blk = s9 >= 4 ? own + (s9 - 4) * 21 : &sm.rec[1 + iy + dy][1 + ix + dx][0] + (4 - s9) * 21;
-      const double* pv = &sm.pub[1 + iy + dy][1 + ix + dx][0];
+      for (int s9 = 0; s9 < 9; ++s9) {
+        if (s9 == 4) continue;
+        const int dx = s9 % 3 - 1, dy = s9 / 3 - 1;
+        const int qa = na + dx, qb = nb + dy;
+        const bool valid = act && qa >= 0 && qa < a.gw && qb >= 0 && qb < a.gh;
+        const bool local = qa >= alo && qa <= ahi && qb >= blo && qb <= bhi;
+        if (!valid || local) continue;
+        const double* blk = s9 >= 4 ? own + (s9 - 4) * 21 : &sm.rec[1 + iy + dy][1 + ix + dx][0] + (4 - s9) * 21;
+        const double* pv = &sm.pub[1 + iy + dy][1 + ix + dx][0];
 #pragma unroll
-      for (int c = 0; c < 6; c += 2) {
-        b0 += blk[ro[c]] * pv[c];
-        b1 += blk[ro[c + 1]] * pv[c + 1];
+        for (int c = 0; c < 6; c += 2) {
+          b0 += blk[ro[c]] * pv[c];
+          b1 += blk[ro[c + 1]] * pv[c + 1];
+        }
+      }
+      b -= b0 + b1;
+    }
+    double m_self = 1.0, m_cross = 0.0;  // solver.cpp:468-474
+    if (act) {
+      const double* pre = own + kSysPre + 3 * (r >> 1);
+      m_self = pre[(r & 1) ? 2 : 0];
+      m_cross = pre[1];
+    }
+    // the staged rows are in registers: reuse the buffer for the next subdomain
+    __syncwarp();
+    if (t + W < total) {
+      T = tile22(a, t + W, nsub);
+      if (u == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before async writes
+        stage22(a, T, sm);
       }
     }
-    b -= b0 + b1;
-  }
-  double m_self = 1.0, m_cross = 0.0;  // solver.cpp:468-474
-  if (act) {
-    const double* pre = own + kSysPre + 3 * (r >> 1);
-    m_self = pre[(r & 1) ? 2 : 0];
-    m_cross = pre[1];
-  }
-  auto apply = [&](double v) {  // local block SpMV (solver.cpp:452-467)
-    __syncwarp();
-    sm.psub[u] = v;
-    __syncwarp();
-    double acc[3] = {0.0, 0.0, 0.0};
+    auto apply = [&](double v) {  // local block SpMV (solver.cpp:452-467)
+      __syncwarp();
+      sm.psub[u] = v;
+      __syncwarp();
+      double acc[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < 4; ++j)
 #pragma unroll
-      for (int c = 0; c < 6; ++c) acc[c % 3] += arow[j][c] * sm.psub[6 * j + c];
-    return act ? (acc[0] + acc[1]) + acc[2] : 0.0;
-  };
-  auto precond = [&](double rv) {
-    const double partner = __shfl_xor_sync(0xffffffffu, rv, 1);
-    return act ? m_self * rv + m_cross * partner : 0.0;
-  };
-  // pcg_impl (solver.cpp:320-361), warm start x0 = published
-  double res = b - apply(x);
-  double z = precond(res);
-  double rz = warp_sum(res * z);
-  const double rz0 = fabs(rz);
-  int flag = 0;
-  if (rz0 != 0.0) {
-    double p = z;
-    for (int it = 0; it < a.pcg_iters; ++it) {
-      const double ap = apply(p);
-      const double pAp = warp_sum(p * ap);
-      if (pAp <= 0.0) {
-        flag = kFlagCurvature;
-        break;
+        for (int c = 0; c < 6; ++c) acc[c % 3] += arow[j][c] * sm.psub[6 * j + c];
+      return act ? (acc[0] + acc[1]) + acc[2] : 0.0;
+    };
+    auto precond = [&](double rv) {
+      const double partner = __shfl_xor_sync(0xffffffffu, rv, 1);
+      return act ? m_self * rv + m_cross * partner : 0.0;
+    };
+    // pcg_impl (solver.cpp:320-361), warm start x0 = published
+    double res = b - apply(x);
+    double z = precond(res);
+    double rz = warp_sum(res * z);
+    const double rz0 = fabs(rz);
+    int flag = 0;
+    if (rz0 != 0.0) {
+      double p = z;
+      for (int it = 0; it < a.pcg_iters; ++it) {
+        const double ap = apply(p);
+        const double pAp = warp_sum(p * ap);
+        if (pAp <= 0.0) {
+          flag = kFlagCurvature;
+          break;
+        }
+        const double alpha = rz / pAp;
+        x += alpha * p;
+        res -= alpha * ap;
+        z = precond(res);
+        const double rzn = warp_sum(res * z);
+        if (fabs(rzn) > 100.0 * rz0) {
+          flag = kFlagGrowth;
+          break;
+        }
+        const double beta = rzn / rz;
+        rz = rzn;
+        p = z + beta * p;
       }
-      const double alpha = rz / pAp;
-      x += alpha * p;
-      res -= alpha * ap;
-      z = precond(res);
-      const double rzn = warp_sum(res * z);
-      if (fabs(rzn) > 100.0 * rz0) {
-        flag = kFlagGrowth;
-        break;
-      }
-      const double beta = rzn / rz;
-      rz = rzn;
-      p = z + beta * p;
     }
-  }
-  if (!act) return;
-  if (flag && u == 0) atomicOr(a.flags + pair, flag);
-  const size_t o = (static_cast<size_t>(pair) * G + n) * 6 + r;
-  if (a.last) {
-    if (!isfinite(x)) atomicOr(a.flags + pair, kFlagStep);
-    if ((a.active >> (r >> 1)) & 1) a.delta[o] += x;
-    a.total[o] = a.base[o] + a.delta[o];
-  } else {
-    a.next[o] = x;
+    if (flag && u == 0) atomicOr(a.flags + pair, flag);
+    if (act) {
+      const size_t o = (static_cast<size_t>(pair) * G + n) * 6 + r;
+      if (a.last) {
+        if (!isfinite(x)) atomicOr(a.flags + pair, kFlagStep);
+        if ((a.active >> (r >> 1)) & 1) a.delta[o] += x;
+        a.total[o] = a.base[o] + a.delta[o];
+      } else {
+        a.next[o] = x;
+      }
+    }
   }
 }
 
@@ -523,7 +556,16 @@ void launch_schwarz(const SwzArgs& a_in, int B, cudaStream_t s) {
     return !e || std::atoi(e) != 0;
   }();
   if (use22 && a.nxm == 2 && a.nym == 2) {
-    k_schwarz22<<<dim3((nsub + 3) / 4, B), 128, 4 * sizeof(Swz22Smem), s>>>(a);
+    static const int grid_cap = [] {
+      int dev = 0, sms = 0, per_sm = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_schwarz22, 128, 4 * sizeof(Swz22Smem));
+      return std::max(1, sms * std::max(per_sm, 1));
+    }();
+    const int total = nsub * B;
+    const int grid = std::min(grid_cap, (total + 3) / 4);
+    k_schwarz22<<<grid, 128, 4 * sizeof(Swz22Smem), s>>>(a, nsub, total);
   } else if (nodes <= 4) {
     k_schwarz<32, 4><<<dim3((nsub + 3) / 4, B), 128, 0, s>>>(a);
   } else if (6 * nodes <= 128) {
