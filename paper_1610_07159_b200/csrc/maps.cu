@@ -309,6 +309,14 @@ __global__ void k_occ_resolve(int w, int h, const int2* __restrict__ q, const fl
     return;
   }
   const double zown = static_cast<double>(Z[pair * N + pix]);
+  // ids of the six triangles incident to x (pin C.2): UL of cells (px,py), (px-1,py), (px,py-1) and LR of
+  // (px-1,py), (px-1,py-1), (px,py-1); a cell outside the lattice gets an id no triangle has
+  const int chh = h - 1;
+  auto cell_id = [&](int cx, int cy, unsigned t) -> unsigned {
+    return (cx >= 0 && cx < cw && cy >= 0 && cy < chh) ? 2u * static_cast<unsigned>(cy * cw + cx) + t : 0xFFFFFFFFu;
+  };
+  const unsigned inc[6] = {cell_id(px, py, 0), cell_id(px - 1, py, 0), cell_id(px, py - 1, 0),
+                            cell_id(px - 1, py, 1), cell_id(px - 1, py - 1, 1), cell_id(px, py - 1, 1)};
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     bool v = !b;
@@ -320,11 +328,8 @@ __global__ void k_occ_resolve(int w, int h, const int2* __restrict__ q, const fl
         const unsigned long long key = zbuf[(static_cast<size_t>(pair) * 4 + e) * N + ry * w + rx];
         if (key != ~0ULL) {
           const unsigned int tri = static_cast<unsigned int>(key & 0xffffffffULL);
-          const int tt = tri & 1, cell = tri >> 1, ccx = cell % cw, ccy = cell / cw;
-          const bool ring = tt == 0 ? ((ccx == px && ccy == py) || (ccx == px - 1 && ccy == py) ||
-                                       (ccx == px && ccy == py - 1))
-                                    : ((ccx == px - 1 && ccy == py) || (ccx == px - 1 && ccy == py - 1) ||
-                                       (ccx == px && ccy == py - 1));
+          const bool ring = tri == inc[0] || tri == inc[1] || tri == inc[2] || tri == inc[3] ||
+                            tri == inc[4] || tri == inc[5];
           if (!ring) {
             const float zf = __uint_as_float(static_cast<unsigned int>(key >> 32));
             if (__dadd_rn(zown, -kDepthTol) > static_cast<double>(zf)) v = false;
