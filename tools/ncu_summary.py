@@ -14,12 +14,17 @@ for r in rows[1:]:
         print(f"  {d['Metric Name']:38s} {d['Metric Value']:>14s} {d.get('Metric Unit','')}")
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rr = list(csv.reader(io.StringIO(raw)))
-hdr, vals = rr[0], rr[2] if len(rr) > 2 else rr[1]
+hdr, units, vals = rr[0], rr[1], (rr[2] if len(rr) > 2 else rr[1])
 m = dict(zip(hdr, vals))
+u = dict(zip(hdr, units))
+SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 def f(k):
     try: return float(m.get(k, "nan").replace(",", ""))
     except ValueError: return float("nan")
-print(f"  dram bytes read+write: {f('dram__bytes_read.sum') + f('dram__bytes_write.sum'):.4g}  (read {f('dram__bytes_read.sum'):.4g} write {f('dram__bytes_write.sum'):.4g})")
+def nbytes(k):
+    return f(k) * SCALE.get(u.get(k, "byte"), 1.0)
+rd, wr = nbytes('dram__bytes_read.sum'), nbytes('dram__bytes_write.sum')
+print(f"  dram bytes read+write: {(rd + wr) / 1e9:.4g} GB  (read {rd / 1e9:.4g} GB, write {wr / 1e9:.4g} GB)")
 stalls = {k: f(k) for k in hdr if k.startswith("smsp__average_warp_latency_issue_stalled") or k.startswith("smsp__pcsamp_warps_issue_stalled")}
 tot = sum(v for k, v in stalls.items() if k.startswith("smsp__pcsamp_warps_issue_stalled") and v == v)
 top = sorted(((v, k) for k, v in stalls.items() if k.startswith("smsp__pcsamp_warps_issue_stalled") and v == v), reverse=True)[:8]
