@@ -334,10 +334,11 @@ def run_ours(args, ws, rank, local):
     l0_ms = sum(t for t, _ in l0) / max(len(l0), 1)
     pk = peaks()
     achieved = big / (l0_ms / 1000.0) / 1e9 if l0_ms > 0 else 0.0  # per launch, algorithmic bytes
-    traffic = None
+    traffic, prof = None, {}
     tf = ROOT / "profiles" / "pixel_traffic.json"
     if tf.exists():  # ncu --set full capture at B=128; DRAM bytes scale with the batch
-        traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch_L0") * B / 128.0
+        prof = json.loads(tf.read_text())
+        traffic = prof.get("dram_bytes_per_launch_L0") * B / 128.0
     launches = lib.hwf_launch_count(h)
 
     # ---- e2e: through the public C-ABI from pinned host buffers ---------------------
@@ -370,7 +371,11 @@ def run_ours(args, ws, rank, local):
                          "frac": achieved / pk["hbm_gbs"] if pk["hbm_gbs"] else None, "traffic": traffic,
                          "kernel": "k_pixel<LIN,U8> (fused data term + cell reduction), finest level, u8 frames sampled directly",
                          "peak_src": pk["src"], "algorithmic_bytes_per_launch": big, "ms_per_launch": l0_ms,
-                         "launches_per_step": nk, "share_of_step": pk_ms / ms_per_step if ms_per_step else None},
+                         "launches_per_step": nk, "share_of_step": pk_ms / ms_per_step if ms_per_step else None,
+                         # not HBM-bound: the limiter and pipe utilisations of the same kernel from the committed
+                         # ncu --set full capture (profiles/pixel_traffic.json)
+                         "limiter": prof.get("limiter"), "fp64_pipe_frac": prof.get("fp64_pipe_frac"),
+                         "l1_lsu_frac": prof.get("l1_lsu_frac"), "issue_slots_frac": prof.get("issue_slots_frac")},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": B * 4 * N,
                     "d2h_bytes_per_step": B * (G * 6 * 8 + N)},
             "gpu_launches": launches * args.steps,
