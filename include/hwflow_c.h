@@ -208,6 +208,13 @@ int hwf_gn_level(hwf_ctx* ctx, const hwf_level* lv, const double* base, double* 
                  uint8_t* outlier, double* node_w, const hwf_energy_params* params,
                  const hwf_schedule* sched, int gn_iters, double* energy_before,
                  double* energy_after);
+/* hwf_gn_level plus SolveSchedule::pcg_trace (solver.hpp:28, solver.cpp:508-513): in global-PCG mode
+ * (subdomain_px = 0), pcg_trace [gn_iters][pcg_iters + 1] receives each iteration's PCG residual
+ * norms (pcg_impl, solver.cpp:331-350); the reference records nothing in Schwarz mode (left as is). */
+int hwf_gn_level_trace(hwf_ctx* ctx, const hwf_level* lv, const double* base, double* delta,
+                       uint8_t* outlier, double* node_w, const hwf_energy_params* params,
+                       const hwf_schedule* sched, int gn_iters, double* energy_before,
+                       double* energy_after, double* pcg_trace);
 /* z-buffer occlusion of the halfway lattice under `total` -> vis4 (N). */
 int hwf_occlusion(hwf_ctx* ctx, int width, int height, int grid_step, const double* total,
                   uint8_t* vis4_out);

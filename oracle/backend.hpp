@@ -32,9 +32,11 @@ struct Backend {
                    double* x, double* trace) = 0;
   virtual void schwarz(int gw, int gh, int step, int tile, int boundary, const double* blocks,
                        const double* rhs, int patch_iters, int pcg_iters, double* x) = 0;
+  // trace (nullable, global-PCG mode): one residual-norm trace per GN iteration (solver.cpp:508-513)
   virtual void gn_level(const hwf_level* lv, const double* base, double* delta, uint8_t* outlier,
                         double* node_w, const hwf_energy_params* P, const hwf_schedule* S,
-                        int gn_iters, std::vector<double>* eb, std::vector<double>* ea) = 0;
+                        int gn_iters, std::vector<double>* eb, std::vector<double>* ea,
+                        std::vector<std::vector<double>>* trace = nullptr) = 0;
 };
 
 Backend* backend();  // defined once per library

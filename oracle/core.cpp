@@ -860,7 +860,7 @@ std::vector<double> schwarz(const System& S, const std::vector<Subdomain>& subs,
 // solver.cpp:484-532
 void gauss_newton(Level L, const double* base, double* delta, uint8_t* outlier, double* node_w,
                   const hwf_schedule& S, int gn_iters, std::vector<double>* e_before,
-                  std::vector<double>* e_after) {
+                  std::vector<double>* e_after, std::vector<std::vector<double>>* pcg_trace) {
   const int G = L.G();
   std::vector<Subdomain> subs;
   if (S.subdomain_px > 0) subs = build_subdomains(L.g.gw, L.g.gh, L.g.step, S.subdomain_px);
@@ -876,9 +876,14 @@ void gauss_newton(Level L, const double* base, double* delta, uint8_t* outlier, 
     const double eb = energy(L, nullptr).total;
     if (e_before) e_before->push_back(eb);
     const System sys = build_normal_system(L, S.active_fields, S.lm_lambda);
-    std::vector<double> step = S.subdomain_px > 0
-                                   ? schwarz(sys, subs, S.patch_iters, S.pcg_iters)
-                                   : pcg_solve(sys, S.pcg_iters, nullptr);
+    std::vector<double> step;
+    if (S.subdomain_px > 0) {
+      step = schwarz(sys, subs, S.patch_iters, S.pcg_iters);
+    } else {  // solver.cpp:508-513
+      std::vector<double> trace;
+      step = pcg_solve(sys, S.pcg_iters, pcg_trace ? &trace : nullptr);
+      if (pcg_trace) pcg_trace->push_back(std::move(trace));
+    }
     for (double v : step)
       if (!std::isfinite(v)) throw Divergence("non-finite Gauss-Newton update");
     for (int n = 0; n < G; ++n)

@@ -141,6 +141,6 @@ void schwarz_sweep(const System& S, const std::vector<Subdomain>& subs, const st
 // rebound internally; delta, outlier and node_w are updated in place.
 void gauss_newton(Level L, const double* base, double* delta, uint8_t* outlier, double* node_w,
                   const hwf_schedule& S, int gn_iters, std::vector<double>* e_before,
-                  std::vector<double>* e_after);
+                  std::vector<double>* e_after, std::vector<std::vector<double>>* pcg_trace = nullptr);
 
 }  // namespace orc

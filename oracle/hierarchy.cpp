@@ -558,15 +558,25 @@ int hwf_schwarz(hwf_ctx* ctx, int gw, int gh, int step, int tile, int boundary, 
     orc::backend()->schwarz(gw, gh, step, tile, boundary, blocks, rhs, patch_iters, pcg_iters, x);
   });
 }
+int hwf_gn_level_trace(hwf_ctx* ctx, const hwf_level* lv, const double* base, double* delta,
+                       uint8_t* outlier, double* node_w, const hwf_energy_params* p,
+                       const hwf_schedule* sched, int gn_iters, double* eb, double* ea, double* pcg_trace) {
+  return orc::guard(ctx, [&] {
+    std::vector<double> b, a;
+    std::vector<std::vector<double>> tr;
+    orc::backend()->gn_level(lv, base, delta, outlier, node_w, p, sched, gn_iters, &b, &a,
+                             pcg_trace && sched->subdomain_px <= 0 ? &tr : nullptr);
+    if (eb) std::memcpy(eb, b.data(), b.size() * sizeof(double));
+    if (ea) std::memcpy(ea, a.data(), a.size() * sizeof(double));
+    const size_t row = static_cast<size_t>(sched->pcg_iters) + 1;
+    for (size_t it = 0; it < tr.size(); ++it)
+      for (size_t k = 0; k < tr[it].size() && k < row; ++k) pcg_trace[it * row + k] = tr[it][k];
+  });
+}
 int hwf_gn_level(hwf_ctx* ctx, const hwf_level* lv, const double* base, double* delta,
                  uint8_t* outlier, double* node_w, const hwf_energy_params* p,
                  const hwf_schedule* sched, int gn_iters, double* eb, double* ea) {
-  return orc::guard(ctx, [&] {
-    std::vector<double> b, a;
-    orc::backend()->gn_level(lv, base, delta, outlier, node_w, p, sched, gn_iters, &b, &a);
-    if (eb) std::memcpy(eb, b.data(), b.size() * sizeof(double));
-    if (ea) std::memcpy(ea, a.data(), a.size() * sizeof(double));
-  });
+  return hwf_gn_level_trace(ctx, lv, base, delta, outlier, node_w, p, sched, gn_iters, eb, ea, nullptr);
 }
 int hwf_occlusion(hwf_ctx* ctx, int w, int h, int step, const double* total, uint8_t* vis4) {
   return orc::guard(ctx, [&] { orc::occlusion(w, h, step, total, vis4); });

@@ -80,9 +80,10 @@ struct Port final : Backend {
   }
   void gn_level(const hwf_level* lv, const double* base, double* delta, uint8_t* outlier,
                 double* node_w, const hwf_energy_params* P, const hwf_schedule* S, int gn_iters,
-                std::vector<double>* eb, std::vector<double>* ea) override {
+                std::vector<double>* eb, std::vector<double>* ea,
+                std::vector<std::vector<double>>* trace) override {
     gauss_newton(make_level(lv, P, S->threads > 0 ? S->threads : 1), base, delta, outlier,
-                 node_w, *S, gn_iters, eb, ea);
+                 node_w, *S, gn_iters, eb, ea, trace);
   }
 };
 

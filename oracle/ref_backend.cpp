@@ -208,7 +208,8 @@ struct Ref final : Backend {
   }
   void gn_level(const hwf_level* lv, const double* base, double* delta, uint8_t* outlier,
                 double* node_w, const hwf_energy_params* P, const hwf_schedule* S, int gn_iters,
-                std::vector<double>* eb, std::vector<double>* ea) override {
+                std::vector<double>* eb, std::vector<double>* ea,
+                std::vector<std::vector<double>>* trace) override {
     guard([&] {
       const int threads = S->threads > 0 ? S->threads : 1;
       RefLevel L(lv, P, threads);
@@ -225,6 +226,7 @@ struct Ref final : Backend {
       s.threads = threads;
       s.lm_lambda = S->lm_lambda;
       s.active_fields = static_cast<uint8_t>(S->active_fields);
+      s.pcg_trace = trace;  // solver.hpp:28
       const hwflow::GnStats st = hwflow::gauss_newton(L.ctx, b, d, L.wts, s, gn_iters);
       from_grid(d, delta);
       std::memcpy(outlier, L.wts.outlier.data(), L.wts.outlier.size());

@@ -124,6 +124,8 @@ _SIGS = {
                               _dp]),
     "hwf_gn_level": (C.c_int, [C.c_void_p, C.POINTER(LevelC), _dp, _dp, _u8p, _dp, C.POINTER(EnergyParamsC),
                                C.POINTER(ScheduleC), C.c_int, _dp, _dp]),
+    "hwf_gn_level_trace": (C.c_int, [C.c_void_p, C.POINTER(LevelC), _dp, _dp, _u8p, _dp, C.POINTER(EnergyParamsC),
+                                     C.POINTER(ScheduleC), C.c_int, _dp, _dp, _dp]),
     "hwf_occlusion": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, _dp, _u8p]),
     "hwf_illumination": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, _dp * 4, _dp, _u8p, _dp]),
     "hwf_prolongate": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _dp, _u8p, _dp, _dp,

@@ -292,7 +292,8 @@ inline void rec_energy_after(LevelDev& d, int B, const hwf_energy_params& P, con
 // The nonlinear loop of one level (solver.cpp:484-532) for a batch, whole level.
 inline void record_gn_level(LevelDev& d, int B, const hwf_energy_params& P, const hwf_schedule& S, const double* dF,
                             int gn, const Energies& E, int slot_base, Scratch& sc, int* flags, cudaStream_t st,
-                            Launches& L, const uint8_t* src8 = nullptr, bool energy_after = true) {
+                            Launches& L, const uint8_t* src8 = nullptr, bool energy_after = true,
+                            double* pcg_trace = nullptr) {  // device [gn][pcg_iters + 1], global mode, B = 1
   for (int it = 0; it < gn; ++it) {
     rec_linearize(d, B, P, S, dF, it, E, slot_base, flags, st, L, src8);
     if (S.subdomain_px > 0) {
@@ -300,7 +301,8 @@ inline void record_gn_level(LevelDev& d, int B, const hwf_energy_params& P, cons
     } else {
       PcgArgs ga{};
       ga.gw = d.gw; ga.gh = d.gh; ga.iters = S.pcg_iters; ga.sys = d.sys;
-      ga.x = sc.px; ga.r = sc.pr; ga.z = sc.pz; ga.p = sc.pp; ga.ap = sc.pap; ga.trace = nullptr; ga.update = 1;
+      ga.x = sc.px; ga.r = sc.pr; ga.z = sc.pz; ga.p = sc.pp; ga.ap = sc.pap; ga.update = 1;
+      ga.trace = pcg_trace ? pcg_trace + static_cast<size_t>(it) * (S.pcg_iters + 1) : nullptr;
       ga.delta = d.delta; ga.total = d.total; ga.base = d.base; ga.active = S.active_fields; ga.flags = flags;
       launch_pcg_global(ga, B, st);
       L.count += 1;

@@ -342,6 +342,13 @@ int hwf_schwarz(hwf_ctx* ctx, int gw, int gh, int step, int tile, int /*boundary
 int hwf_gn_level(hwf_ctx* ctx, const hwf_level* lv, const double* base, double* delta, uint8_t* outlier,
                  double* node_w, const hwf_energy_params* P, const hwf_schedule* S, int gn_iters,
                  double* energy_before, double* energy_after) {
+  return hwf_gn_level_trace(ctx, lv, base, delta, outlier, node_w, P, S, gn_iters, energy_before, energy_after,
+                            nullptr);
+}
+
+int hwf_gn_level_trace(hwf_ctx* ctx, const hwf_level* lv, const double* base, double* delta, uint8_t* outlier,
+                       double* node_w, const hwf_energy_params* P, const hwf_schedule* S, int gn_iters,
+                       double* energy_before, double* energy_after, double* pcg_trace) {
   return guard(ctx, [&] {
     check_params(P, S, lv->fundamental);
     if (gn_iters < 0 || gn_iters > HWF_MAX_GN) throw InvalidArg("bad gn_iters");
@@ -363,7 +370,10 @@ int hwf_gn_level(hwf_ctx* ctx, const hwf_level* lv, const double* base, double* 
     Scratch sc;
     sc.alloc(m, 1, d.N, d.G, false, false, S->subdomain_px <= 0);
     Launches LC;
-    record_gn_level(d, 1, *P, *S, dF, gn_iters, E, 0, sc, flags, ctx->stream, LC);
+    const bool traced = pcg_trace && S->subdomain_px <= 0 && gn_iters > 0;
+    const size_t trace_n = static_cast<size_t>(gn_iters) * (S->pcg_iters + 1);
+    double* dtrace = traced ? up<double>(m, nullptr, trace_n) : nullptr;
+    record_gn_level(d, 1, *P, *S, dF, gn_iters, E, 0, sc, flags, ctx->stream, LC, nullptr, true, dtrace);
     launch_energy_reduce(E.part, E.nslots, E.cap, 1, E.red, flags, ctx->stream);
     CK(cudaStreamSynchronize(ctx->stream));
     CK(cudaGetLastError());
@@ -379,6 +389,7 @@ int hwf_gn_level(hwf_ctx* ctx, const hwf_level* lv, const double* base, double* 
     down(delta, d.delta, 6 * d.G);
     down(outlier, d.W, d.N);
     down(node_w, d.nodew, d.G);
+    if (traced) down(pcg_trace, dtrace, trace_n);
     check_flags(flags);
   });
 }

@@ -425,16 +425,21 @@ class Solver:
         return x
 
     def gauss_newton(self, lv: LevelState, base: np.ndarray, params: EnergyParams, schedule: SolveSchedule,
-                     gn_iters: int):
-        """solver.cpp:484-532; returns (delta, outlier, node_w, energy_before, energy_after)."""
+                     gn_iters: int, pcg_trace: bool = False):
+        """solver.cpp:484-532; returns (delta, outlier, node_w, energy_before, energy_after), plus the
+        per-iteration PCG residual-norm traces (gn_iters, pcg_iters + 1) when pcg_trace (global-PCG mode,
+        SolveSchedule::pcg_trace, solver.cpp:508-513)."""
         c, pc, sc = lv.to_c(), params.to_c(), schedule.to_c()
         base = np.ascontiguousarray(base, np.float64).reshape(-1, 6)
         delta = lv.delta.copy()
         W, nw = lv.outlier.copy(), lv.node_w.copy()
         eb, ea = np.empty(max(gn_iters, 1)), np.empty(max(gn_iters, 1))
-        self.ctx.check(self.lib.hwf_gn_level(self.ctx.h, C.byref(c), dptr(base), dptr(delta), u8ptr(W), dptr(nw),
-                                             C.byref(pc), C.byref(sc), gn_iters, dptr(eb), dptr(ea)))
-        return delta, W, nw, eb[:gn_iters], ea[:gn_iters]
+        tr = np.zeros((max(gn_iters, 1), schedule.pcg_iters + 1)) if pcg_trace else None
+        self.ctx.check(self.lib.hwf_gn_level_trace(self.ctx.h, C.byref(c), dptr(base), dptr(delta), u8ptr(W),
+                                                   dptr(nw), C.byref(pc), C.byref(sc), gn_iters, dptr(eb), dptr(ea),
+                                                   dptr(tr)))
+        out = (delta, W, nw, eb[:gn_iters], ea[:gn_iters])
+        return out + (tr[:gn_iters],) if pcg_trace else out
 
     def compute_occlusion_maps(self, w: int, h: int, step: int, total: np.ndarray) -> np.ndarray:
         t = np.ascontiguousarray(total, np.float64)

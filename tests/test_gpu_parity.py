@@ -118,6 +118,17 @@ def test_gauss_newton_level_matches_reference_golden(device, golden, mode, sub):
     np.testing.assert_allclose(ea, golden[f"gn_{mode}_ea"], rtol=ENERGY_RTOL)
 
 
+def test_gauss_newton_pcg_trace_matches_oracle(device, oracle, golden):
+    """SolveSchedule::pcg_trace in global mode (solver.cpp:508-513) through hwf_gn_level_trace."""
+    gw, gh = grid_dims(40, 32, 8)
+    lv = LevelState(golden["gn_images"], 8, np.zeros((gw * gh, 6)), np.zeros((gw * gh, 6)))
+    S = SolveSchedule(levels=1, grid_step=8, pcg_iters=5, subdomain_px=0)
+    a = device.gauss_newton(lv, np.zeros((gw * gh, 6)), EnergyParams(), S, 3, pcg_trace=True)
+    b = oracle.gauss_newton(lv, np.zeros((gw * gh, 6)), EnergyParams(), S, 3, pcg_trace=True)
+    np.testing.assert_allclose(a[5], b[5], rtol=1e-6)  # norms after 3 GN iterations of an ill-conditioned level
+    np.testing.assert_allclose(a[5][0], b[5][0], rtol=1e-9)
+
+
 # ---- occlusion (bit-exact on identical input flows), illumination, prolongation --------
 def _wavy_total(seed, w, h, step, amp):
     rng = np.random.default_rng(seed)

@@ -264,3 +264,16 @@ def test_jacobian_finite_differences_oracle():
     picks = [(int(rng.integers(G)), int(rng.integers(6))) for _ in range(24)]
     errs = gp._fd_jacobian_check(orc, lv, EnergyParams.preset("facial"), picks)
     assert np.median(errs) < 1e-5 and (errs < 1e-3).mean() >= 0.9, errs
+
+
+def test_gn_pcg_trace_port_matches_reference(oracle, reference, golden):
+    """SolveSchedule::pcg_trace (solver.hpp:28, solver.cpp:508-513): one PCG residual-norm trace per GN
+    iteration in global mode; the restatement against the reference build."""
+    gw, gh = grid_dims(40, 32, 8)
+    lv = LevelState(golden["gn_images"], 8, np.zeros((gw * gh, 6)), np.zeros((gw * gh, 6)))
+    S = SolveSchedule(levels=1, grid_step=8, pcg_iters=5, subdomain_px=0)
+    a = oracle.gauss_newton(lv, np.zeros((gw * gh, 6)), EnergyParams(), S, 3, pcg_trace=True)
+    b = reference.gauss_newton(lv, np.zeros((gw * gh, 6)), EnergyParams(), S, 3, pcg_trace=True)
+    assert a[5].shape == (3, 6)
+    np.testing.assert_allclose(a[5], b[5], rtol=1e-12)
+    assert a[5][0, 0] > a[5][0, -1] > 0.0
