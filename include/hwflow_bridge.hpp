@@ -115,8 +115,14 @@ inline GnStats gauss_newton(const Device& dev, EnergyContext& ctx, const WarpGri
   const hwf_energy_params p = to_c(ctx.params);
   const hwf_schedule s = to_c(sched);
   std::vector<double> eb(gn_iters), ea(gn_iters);
-  check(dev.get(), hwf_gn_level(dev.get(), &lv, b.data(), d.data(), weights.outlier.data(), weights.node_w.data(),
-                                &p, &s, gn_iters, eb.data(), ea.data()));
+  const bool traced = sched.pcg_trace && sched.subdomain_px <= 0;  // solver.cpp:508-513
+  const size_t row = static_cast<size_t>(sched.pcg_iters) + 1;
+  std::vector<double> tr(traced ? row * gn_iters : 0);
+  check(dev.get(), hwf_gn_level_trace(dev.get(), &lv, b.data(), d.data(), weights.outlier.data(),
+                                      weights.node_w.data(), &p, &s, gn_iters, eb.data(), ea.data(),
+                                      traced ? tr.data() : nullptr));
+  if (traced)
+    for (int it = 0; it < gn_iters; ++it) sched.pcg_trace->emplace_back(tr.begin() + it * row, tr.begin() + (it + 1) * row);
   grid_from_c(d, delta);
   GnStats st;
   st.energy_before = eb;
