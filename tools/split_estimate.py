@@ -1,0 +1,119 @@
+"""Per-rank device time of the 4K strip split (include/hwflow_split.h), measured on ONE GPU.
+
+The world's ranks run in this process with LocalComm, all on one context (one stream). Every
+step call of every rank is bracketed with CUDA events, so each rank's busy time is measured on the
+device. The halo and all-gather copies are not counted here. The exchanged bytes are counted, and
+the script prints a projected N-GPU frame time: max over ranks of busy time, plus the exchanges
+at an assumed NVLink rate and per-collective latency. This is an estimate, labelled as such. With
+one GPU per gpurun call, multi-GPU runs cannot be measured here.
+
+    python tools/split_estimate.py --worlds 1 2 4 8
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import torch  # noqa: E402
+
+from paper_1610_07159_b200 import build, synthetic  # noqa: E402
+from paper_1610_07159_b200.capi import DTYPE_U8  # noqa: E402
+from paper_1610_07159_b200.hwflow import EnergyParams, SolveSchedule, Solver  # noqa: E402
+from paper_1610_07159_b200.split import LocalComm, SplitRank, solve_split  # noqa: E402
+
+NVLINK_GBS = 700.0      # assumed effective NVLink 5 P2P / all-gather rate per GPU (B200 spec: 900 GB/s/dir)
+LATENCY_US = 15.0       # assumed per-collective latency
+
+
+class Timed(SplitRank):
+    def __init__(self, *a, **k):
+        super().__init__(*a, **k)
+        self.ms = 0.0
+
+    def _t(self, fn, *args):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(self.stream)
+        fn(*args)
+        e1.record(self.stream)
+        self._ev.append((e0, e1))
+
+    def begin(self, f):
+        self._ev = []
+        self._t(super().begin, f)
+
+    def level_begin(self, l):
+        self._t(super().level_begin, l)
+
+    def linearize(self, l, it):
+        self._t(super().linearize, l, it)
+
+    def sweep(self, l, s):
+        self._t(super().sweep, l, s)
+
+    def energy_after(self, l):
+        self._t(super().energy_after, l)
+
+    def level_end(self, l):
+        self._t(super().level_end, l)
+
+    def finish(self):
+        torch.cuda.synchronize()
+        self.ms = sum(a.elapsed_time(b) for a, b in self._ev)
+        return super().finish()
+
+
+class CountingComm(LocalComm):
+    def __init__(self):
+        self.halo_bytes = self.gather_bytes = 0
+        self.halos = self.gathers = 0
+
+    def halo(self, ranks, level, name):
+        gw = ranks[0].rows[level][2]
+        self.halo_bytes += 2 * 6 * gw * 8  # one row each way per boundary, per rank (upper bound)
+        self.halos += 1
+        super().halo(ranks, level, name)
+
+    def allgather_rows(self, ranks, level, name):
+        gw = ranks[0].rows[level][2]
+        gh = max(r.rows[level][1] for r in ranks)
+        self.gather_bytes += 6 * gw * gh * 8  # every rank receives the whole grid
+        self.gathers += 1
+        super().allgather_rows(ranks, level, name)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--worlds", type=int, nargs="+", default=[1, 2, 4, 8])
+    ap.add_argument("--reps", type=int, default=3)
+    a = ap.parse_args()
+    dev = Solver(build.CUDA_LIB)
+    imgs = synthetic.uhd_pair(0)[0]
+    S = SolveSchedule(levels=5, grid_step=4, pcg_iters=5, patch_iters=5, subdomain_px=16)
+    h, w = imgs.shape[1:]
+    out = []
+    for world in a.worlds:
+        ranks = [Timed(dev, w, h, DTYPE_U8, EnergyParams(), S, None, r, world) for r in range(world)]
+        for _ in range(a.reps):  # last rep counts
+            comm = CountingComm()
+            solve_split(ranks, comm, imgs)
+        busy = [r.ms for r in ranks]
+        xfer_ms = (comm.halo_bytes + comm.gather_bytes) / (NVLINK_GBS * 1e9) * 1e3
+        lat_ms = (comm.halos + comm.gathers) * LATENCY_US / 1e3 if world > 1 else 0.0
+        proj = max(busy) + (xfer_ms + lat_ms if world > 1 else 0.0)
+        row = {"world": world, "rank_busy_ms": [round(b, 3) for b in busy], "max_busy_ms": round(max(busy), 3),
+               "exchanges": comm.halos + comm.gathers, "exchange_MB": round((comm.halo_bytes + comm.gather_bytes) / 1e6, 2),
+               "projected_frame_ms": round(proj, 3), "projected_hz": round(1000.0 / proj, 1)}
+        out.append(row)
+        print(json.dumps(row), flush=True)
+        for r in ranks:
+            r.close()
+    return out
+
+
+if __name__ == "__main__":
+    main()
