@@ -425,13 +425,15 @@ __global__ void k_prolong_maps(int wc, int hc, int wf, int hf, const uint8_t* __
   const int x1 = min(cx.i0 + 1, wc - 1), y1 = min(cy.i0 + 1, hc - 1);
   const uint8_t q00 = V[static_cast<size_t>(cy.i0) * wc + cx.i0], q10 = V[static_cast<size_t>(cy.i0) * wc + x1];
   const uint8_t q01 = V[static_cast<size_t>(y1) * wc + cx.i0], q11 = V[static_cast<size_t>(y1) * wc + x1];
-  const double fx = cx.f, fy = cy.f;
+  // x / 2 leaves fractions in {0, 1/2, 1}, so the bilinear weights are quarters and the test
+  // sum >= 0.5 is exact in integers: 4 * sum >= 2 (pin C.3)
+  const int fx2 = static_cast<int>(cx.f * 2.0), fy2 = static_cast<int>(cy.f * 2.0);
+  const int w00 = (2 - fx2) * (2 - fy2), w10 = fx2 * (2 - fy2), w01 = (2 - fx2) * fy2, w11 = fx2 * fy2;
   uint8_t bits = 0;
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    const double v = (1 - fx) * (1 - fy) * ((q00 >> e) & 1) + fx * (1 - fy) * ((q10 >> e) & 1) +
-                     (1 - fx) * fy * ((q01 >> e) & 1) + fx * fy * ((q11 >> e) & 1);
-    if (v >= 0.5) bits |= static_cast<uint8_t>(1u << e);
+    const int v4 = w00 * ((q00 >> e) & 1) + w10 * ((q10 >> e) & 1) + w01 * ((q01 >> e) & 1) + w11 * ((q11 >> e) & 1);
+    if (v4 >= 2) bits |= static_cast<uint8_t>(1u << e);
   }
   vf[pair * Nf + pix] = bits;
   if (hmc && illf) {
