@@ -373,22 +373,30 @@ __global__ void k_illum_resid(int w, int h, int gw, int gh, int step, const doub
   }
 }
 
+// Separable Gaussian (image.cpp:124-155), taps summed in the reference's order i = -R..R.
+// The radius is pinned (sigma 3.2 -> R = 10), so the tap loop is unrolled; R_ < 0 reads it at run time.
+constexpr int kBlurR = 10;
+int g_gauss_r = -1;  // host copy of c_gauss_r (init_maps_constants)
+template <int R_>
 __global__ void k_blur_h(int w, int h, const double* __restrict__ src, double* __restrict__ dst) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y, plane = blockIdx.z;
   if (x >= w) return;
   const double* S = src + static_cast<size_t>(plane) * w * h + static_cast<size_t>(y) * w;
-  const int R = c_gauss_r;
+  const int R = R_ >= 0 ? R_ : c_gauss_r;
   double acc = 0.0;
+#pragma unroll
   for (int i = -R; i <= R; ++i) acc += c_gauss[i + R] * __ldg(S + min(max(x + i, 0), w - 1));
   dst[static_cast<size_t>(plane) * w * h + static_cast<size_t>(y) * w + x] = acc;
 }
 
+template <int R_>
 __global__ void k_blur_v_half(int w, int h, const double* __restrict__ src, double* __restrict__ dst) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y, plane = blockIdx.z;
   if (x >= w) return;
   const double* S = src + static_cast<size_t>(plane) * w * h;
-  const int R = c_gauss_r;
+  const int R = R_ >= 0 ? R_ : c_gauss_r;
   double acc = 0.0;
+#pragma unroll
   for (int i = -R; i <= R; ++i) acc += c_gauss[i + R] * __ldg(S + static_cast<size_t>(min(max(y + i, 0), h - 1)) * w + x);
   dst[static_cast<size_t>(plane) * w * h + static_cast<size_t>(y) * w + x] = 0.5 * acc;  // +-blur/2 split
 }
@@ -524,6 +532,7 @@ void init_maps_constants() {
   for (int i = 0; i < 2 * R + 1; ++i) k[i] /= sum;
   cudaMemcpyToSymbol(c_gauss, k, sizeof(double) * (2 * R + 1));
   cudaMemcpyToSymbol(c_gauss_r, &R, sizeof(int));
+  g_gauss_r = R;
 }
 void launch_pyr_in(const void* src, int dtype, double* dst, long long n, cudaStream_t s) {
   k_pyr_in<<<static_cast<unsigned>((n + kThreads - 1) / kThreads), kThreads, 0, s>>>(src, dtype, dst, n);
@@ -556,8 +565,13 @@ void launch_occlusion(int w, int h, int gw, int gh, int step, const double* tota
 void launch_illumination(int w, int h, int gw, int gh, int step, const double* img, const double* total,
                          const uint8_t* vis, int B, double* resid, double* tmp, double* hm, cudaStream_t s) {
   k_illum_resid<<<rows_grid(w, h, B), kThreads, 0, s>>>(w, h, gw, gh, step, img, total, vis, resid);
-  k_blur_h<<<rows_grid(w, h, 2 * B), kThreads, 0, s>>>(w, h, resid, tmp);
-  k_blur_v_half<<<rows_grid(w, h, 2 * B), kThreads, 0, s>>>(w, h, tmp, hm);
+  if (g_gauss_r == kBlurR) {
+    k_blur_h<kBlurR><<<rows_grid(w, h, 2 * B), kThreads, 0, s>>>(w, h, resid, tmp);
+    k_blur_v_half<kBlurR><<<rows_grid(w, h, 2 * B), kThreads, 0, s>>>(w, h, tmp, hm);
+  } else {
+    k_blur_h<-1><<<rows_grid(w, h, 2 * B), kThreads, 0, s>>>(w, h, resid, tmp);
+    k_blur_v_half<-1><<<rows_grid(w, h, 2 * B), kThreads, 0, s>>>(w, h, tmp, hm);
+  }
 }
 void launch_prolong_grid(int gwc, int ghc, int gwf, int ghf, int step, const double* total_c, double* base_f,
                          double* total_f, double* delta_f, int B, cudaStream_t s) {
