@@ -165,16 +165,16 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm)}
 
 
-def cpu_baseline(steps: int, warmup: int, mode: str) -> dict:
+def cpu_baseline(steps: int, warmup: int, mode: str, threads: int | None = None) -> dict:
     """The reference's CPU path (oracle/_ref: reference sources + SPEC-restated hierarchy),
-    all host threads, one cfg2 pair per step. Falls back to the oracle port."""
+    all host threads (or `threads`), one cfg2 pair per step. Falls back to the oracle port."""
     from paper_1610_07159_b200 import build
     from paper_1610_07159_b200.hwflow import EnergyParams, Solver
     lib, kind = (build.REF_LIB, "reference") if build.REF_LIB.exists() else (build.ORACLE_LIB, "port")
     if not lib.exists():
         build.build_oracle()
     cpu = Solver(lib)
-    cores = os.cpu_count() or 1
+    cores = threads or os.cpu_count() or 1
     sched = schedule(mode)
     sched.threads = cores
     frames = make_frames(max(steps, 1), 0)
@@ -358,6 +358,7 @@ def run_ours(args, ws, rank, local):
     extra = extra_configs(dev, lib, h, C, capi) if (rank == 0 and ws == 1 and not args.no_extra) else None
     if rank == 0:
         cb = cpu_baseline(max(1, min(3, args.steps)), 1, args.mode) if ws == 1 and not args.no_cpu else None
+        cb1 = cpu_baseline(1, 0, args.mode, threads=1) if ws == 1 and not args.no_cpu else None
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
@@ -384,6 +385,7 @@ def run_ours(args, ws, rank, local):
         }
         if cb:
             line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            line["cpu_baseline"]["single_thread"] = {k: cb1[k] for k in ("value", "cores", "sample")}
         if extra:
             line["other_configs"] = extra
         print(json.dumps(line), flush=True)
