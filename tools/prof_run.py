@@ -21,9 +21,12 @@ ap.add_argument("--batch", type=int, default=8)
 ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--runs", type=int, default=1)
 ap.add_argument("--mode", default="schwarz")
+ap.add_argument("--profiling", action="store_true", help="plans with in-graph k_pixel<LIN> timing events")
 a = ap.parse_args()
 
 dev = Solver(build.CUDA_LIB)
+if a.profiling:
+    dev.lib.hwf_set_profiling(dev.ctx.h, 1)
 frames = make_frames(a.batch, 0)
 P, S = EnergyParams(), schedule(a.mode)
 outs, _ = None, None
