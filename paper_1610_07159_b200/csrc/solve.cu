@@ -230,6 +230,18 @@ struct alignas(16) Swz22Smem {
   uint64_t bar;
 };
 
+// a / b for the PCG step lengths: the hardware reciprocal estimate refined by two Newton steps
+// (error ~1 ulp against the correctly rounded quotient; no libdevice slow-path branch)
+__device__ __forceinline__ double fdiv(double a, double b) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
+  double e = __fma_rn(-b, r, 1.0);
+  r = __fma_rn(r, e, r);
+  e = __fma_rn(-b, r, 1.0);
+  r = __fma_rn(r, e, r);
+  return a * r;
+}
+
 struct Tile22 {  // one subdomain of the launch's range
   int pair, alo, ahi, blo, bhi;
 };
@@ -389,7 +401,7 @@ __global__ void __launch_bounds__(128) k_schwarz22(const SwzArgs a, int nsub, in
           flag = kFlagCurvature;
           break;
         }
-        const double alpha = rz / pAp;
+        const double alpha = fdiv(rz, pAp);
         x += alpha * p;
         res -= alpha * ap;
         z = precond(res);
@@ -398,7 +410,7 @@ __global__ void __launch_bounds__(128) k_schwarz22(const SwzArgs a, int nsub, in
           flag = kFlagGrowth;
           break;
         }
-        const double beta = rzn / rz;
+        const double beta = fdiv(rzn, rz);
         rz = rzn;
         p = z + beta * p;
       }
