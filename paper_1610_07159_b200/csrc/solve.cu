@@ -362,14 +362,13 @@ __global__ void __launch_bounds__(128) k_schwarz22(const SwzArgs a, int nsub, in
       m_self = pre[(r & 1) ? 2 : 0];
       m_cross = pre[1];
     }
-    // the staged rows are in registers: reuse the buffer for the next subdomain
+    // the staged rows are in registers: reuse the buffer for the next subdomain. Every lane orders its
+    // generic reads of the buffer before the async-proxy writes of the next copies, then the warp syncs.
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (t + W < total) {
       T = tile22(a, t + W, nsub);
-      if (u == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before async writes
-        stage22(a, T, sm);
-      }
+      if (u == 0) stage22(a, T, sm);
     }
     auto apply = [&](double v) {  // local block SpMV (solver.cpp:452-467)
       __syncwarp();
