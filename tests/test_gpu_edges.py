@@ -94,3 +94,36 @@ def test_invalid_inputs_are_einval(device):
             device.solve_batch(frames, params, sched, F)
     (r,), _ = device.solve_batch(imgs[None], P, S)  # the context is still usable afterwards
     assert np.isfinite(r.grid_total).all()
+
+
+def test_c_abi_nulls_and_limits(device):
+    """C-level argument checks (the reference's std::invalid_argument cases) and the schedule maxima."""
+    import ctypes as C
+
+    from paper_1610_07159_b200 import capi
+    lib, h = device.lib, device.ctx.h
+    imgs = synthetic.constant_pair(32, 24)[0]
+    P, S = EnergyParams().to_c(), SolveSchedule(levels=2, grid_step=8).to_c()
+    fr = capi.Frame4C()
+    fr.width, fr.height, fr.dtype = 32, 24, capi.DTYPE_U8
+    keep = np.ascontiguousarray(imgs)
+    for e in range(4):
+        fr.plane[e] = keep[e].ctypes.data
+    out = capi.ResultC()
+    st = capi.StatsC()
+    assert lib.hwf_solve_pair(h, None, C.byref(P), C.byref(S), None, C.byref(out), C.byref(st)) == capi.HWF_EINVAL
+    assert lib.hwf_solve_pair(h, C.byref(fr), None, C.byref(S), None, C.byref(out), C.byref(st)) == capi.HWF_EINVAL
+    assert lib.hwf_solve_pair(h, C.byref(fr), C.byref(P), None, None, C.byref(out), C.byref(st)) == capi.HWF_EINVAL
+    fr.plane[2] = None
+    assert lib.hwf_solve_pair(h, C.byref(fr), C.byref(P), C.byref(S), None, C.byref(out), C.byref(st)) == capi.HWF_EINVAL
+    assert "plane" in lib.hwf_last_error(h).decode()
+    fr.plane[2] = keep[2].ctypes.data
+    S_many = SolveSchedule(levels=2, grid_step=8, gn_per_level=[33]).to_c()
+    assert lib.hwf_solve_pair(h, C.byref(fr), C.byref(P), C.byref(S_many), None, C.byref(out), C.byref(st)) == capi.HWF_EINVAL
+    # the maxima themselves run: 8 levels requested (auto-reduced), 32 GN iterations at a level
+    S_max = SolveSchedule(levels=8, grid_step=8, gn_per_level=[32, 1], pcg_iters=2, subdomain_px=0).to_c()
+    g = np.empty((5 * 4, 6))
+    out.grid_total = g.ctypes.data_as(capi._dp)
+    assert lib.hwf_solve_pair(h, C.byref(fr), C.byref(P), C.byref(S_max), None, C.byref(out), C.byref(st)) in (
+        capi.HWF_OK, capi.HWF_EDIVERGED)
+    assert st.levels_used >= 1 and st.gn_iters[0] == 32
