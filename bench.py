@@ -90,6 +90,29 @@ def extra_configs(dev, lib, h, C, capi, reps: int = 5) -> dict:
         ms = e0.elapsed_time(e1) / reps
         out[name] = {"pairs": n, "ms_per_step": ms, "pairs_per_s": 1000.0 * n / ms,
                      "solver_status": status, "launches_per_step": lib.hwf_launch_count(h)}
+    # live sequences, each step warm-started from the previous frame's device-resident
+    # hierarchy (hwf_solve_batch_seq; states ping-pong), 16 parallel sequences of 640x480, host in/out; global
+    # PCG (the reference's Schwarz mode diverges on these noise-free constant-velocity scenes, as in the tests)
+    nseq, steps = 16, 3
+    per_seq = [synthetic.sequence_pairs(steps, W_, H_, seed=1610 + i) for i in range(nseq)]
+    frames = [np.ascontiguousarray(np.stack([per_seq[i][k] for i in range(nseq)])) for k in range(steps)]
+    if True:
+        S = SolveSchedule(levels=4, grid_step=8, pcg_iters=5, subdomain_px=0)
+        st = [dev.new_state(nseq, W_, H_, S), dev.new_state(nseq, W_, H_, S)]
+        status = "ok"
+        try:
+            dev.solve_batch_seq(frames[0], EnergyParams(), S, None, st[0], outputs=("grid_total",))
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for k in range(1, len(frames)):
+                dev.solve_batch_seq(frames[k], EnergyParams(), S, st[(k - 1) % 2], st[k % 2], outputs=("grid_total",))
+            dt = (time.perf_counter() - t0) / (len(frames) - 1)
+        except capi.SolverDivergence:
+            status, dt = "diverged-flag", float("nan")
+        out["cfg2_sequence_warm_start_global_pcg_16x"] = {"pairs": nseq, "ms_per_step": 1000.0 * dt,
+                                               "pairs_per_s": nseq / dt if dt == dt else None,
+                                               "solver_status": status,
+                                               "note": "wall clock per step incl. H2D of u8 frames and D2H of the grid"}
     return out
 
 
