@@ -16,9 +16,12 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "launch.h"
 
 namespace hwf {
+namespace cg = cooperative_groups;
 namespace {
 
 // Row r of block(n, slot9) of the symmetric system.
@@ -547,6 +550,138 @@ __global__ void __launch_bounds__(kPcgThreads) k_pcg_global(const PcgArgs a) {
   }
 }
 
+// ---- k_pcg_cluster: the same global PCG with a thread-block cluster per pair -------------------------
+// k_pcg_global runs one CTA per pair, so a batch smaller than the SM count leaves most of the GPU idle.
+// Here a cluster of kPcgCluster CTAs shares one pair. Each CTA owns a contiguous node slice of every
+// vector. Dots reduce per CTA in a fixed order, then every CTA sums the kPcgCluster partials in rank
+// order through distributed shared memory, so all CTAs hold the same bits. Cluster barriers
+// (release/acquire) make each CTA's slice of p visible to the others' SpMV.
+constexpr int kPcgCluster = 8, kPcgClusterThreads = 256;
+
+__device__ double slice_dot(const double* __restrict__ x, const double* __restrict__ y, int lo, int hi, double* red,
+                            double* part, cg::cluster_group& cl) {
+  double s = 0.0;
+  for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) s += x[i] * y[i];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
+    *part = t;
+  }
+  cl.sync();
+  double tot = 0.0;
+  for (int k = 0; k < kPcgCluster; ++k) tot += *cl.map_shared_rank(part, k);
+  return tot;
+}
+
+__global__ void __cluster_dims__(kPcgCluster, 1, 1) __launch_bounds__(kPcgClusterThreads)
+    k_pcg_cluster(const PcgArgs a) {
+  __shared__ double red[kPcgClusterThreads / 32];
+  __shared__ double part[2];  // alternating dot partials (a partial is rewritten two dots later)
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = static_cast<int>(cl.block_rank());
+  const int pair = blockIdx.x / kPcgCluster;
+  const int G = a.gw * a.gh, M = 6 * G;
+  const int lo = 6 * static_cast<int>(static_cast<long long>(G) * rank / kPcgCluster);
+  const int hi = 6 * static_cast<int>(static_cast<long long>(G) * (rank + 1) / kPcgCluster);
+  const double* sys = a.sys + static_cast<size_t>(pair) * G * kSysStride;
+  double* x = a.x + static_cast<size_t>(pair) * M;
+  double* r = a.r + static_cast<size_t>(pair) * M;
+  double* z = a.z + static_cast<size_t>(pair) * M;
+  double* p = a.p + static_cast<size_t>(pair) * M;
+  double* ap = a.ap + static_cast<size_t>(pair) * M;
+  double* tr = a.trace ? a.trace + static_cast<size_t>(pair) * (a.iters + 1) : nullptr;
+  int nd = 0;  // dots issued (selects the partial slot)
+  auto dot = [&](const double* u, const double* v) { return slice_dot(u, v, lo, hi, red, &part[nd++ & 1], cl); };
+  auto spmv_slice = [&](const double* xv, double* y) {  // rows [lo, hi) of the 9-slot block SpMV
+    for (int t = lo + threadIdx.x; t < hi; t += blockDim.x) {
+      const int n = t / 6, rr = t % 6, na = n % a.gw, nb = n / a.gw;
+      double acc = 0.0;
+      for (int s9 = 0; s9 < 9; ++s9) {
+        const int qa = na + s9 % 3 - 1, qb = nb + s9 / 3 - 1;
+        if (qa < 0 || qa >= a.gw || qb < 0 || qb >= a.gh) continue;
+        const int qn = qb * a.gw + qa;
+        for (int c = 0; c < 6; ++c) acc += sys_entry(sys, G, n, qn, s9, rr, c) * xv[6 * qn + c];
+      }
+      y[t] = acc;
+    }
+  };
+  auto precond_slice = [&]() {
+    for (int t = lo + threadIdx.x; t < hi; t += blockDim.x) {
+      const int n = t / 6, k = t % 6;
+      const double* pre = sys + static_cast<size_t>(n) * kSysStride + kSysPre + 3 * (k >> 1);
+      const int e = t & ~1;
+      z[t] = (k & 1) ? pre[1] * r[e] + pre[2] * r[e + 1] : pre[0] * r[e] + pre[1] * r[e + 1];
+    }
+  };
+  for (int t = lo + threadIdx.x; t < hi; t += blockDim.x) {
+    x[t] = 0.0;
+    r[t] = __ldg(sys + static_cast<size_t>(t / 6) * kSysStride + kSysRhs + t % 6);
+  }
+  __syncthreads();
+  if (tr) {
+    const double nr = dot(r, r);
+    if (rank == 0 && threadIdx.x == 0) tr[0] = sqrt(nr);
+  }
+  precond_slice();
+  __syncthreads();
+  double rz = dot(r, z);
+  const double rz0 = fabs(rz);
+  int flag = 0;
+  if (rz0 == 0.0) {
+    if (tr && rank == 0 && threadIdx.x == 0)
+      for (int it = 0; it < a.iters; ++it) tr[it + 1] = 0.0;
+  } else {
+    for (int t = lo + threadIdx.x; t < hi; t += blockDim.x) p[t] = z[t];
+    cl.sync();  // every slice of p is written before any SpMV reads it
+    for (int it = 0; it < a.iters; ++it) {
+      spmv_slice(p, ap);
+      __syncthreads();
+      const double pAp = dot(p, ap);
+      if (pAp <= 0.0) {
+        flag = kFlagCurvature;
+        break;
+      }
+      const double alpha = rz / pAp;
+      for (int t = lo + threadIdx.x; t < hi; t += blockDim.x) {
+        x[t] += alpha * p[t];
+        r[t] -= alpha * ap[t];
+      }
+      __syncthreads();
+      if (tr) {
+        const double nr = dot(r, r);
+        if (rank == 0 && threadIdx.x == 0) tr[it + 1] = sqrt(nr);
+      }
+      precond_slice();
+      __syncthreads();
+      const double rzn = dot(r, z);
+      if (fabs(rzn) > 100.0 * rz0) {
+        flag = kFlagGrowth;
+        break;
+      }
+      const double beta = rzn / rz;
+      rz = rzn;
+      // (every slice's SpMV of this iteration read p before the pAp dot's cluster barrier)
+      for (int t = lo + threadIdx.x; t < hi; t += blockDim.x) p[t] = z[t] + beta * p[t];
+      cl.sync();  // the new p is complete
+    }
+  }
+  if (flag && rank == 0 && threadIdx.x == 0) atomicOr(a.flags + pair, flag);
+  if (a.update) {
+    const size_t o = static_cast<size_t>(pair) * M;
+    bool bad = false;
+    for (int t = lo + threadIdx.x; t < hi; t += blockDim.x) {
+      bad = bad || !isfinite(x[t]);
+      if ((a.active >> ((t % 6) >> 1)) & 1) a.delta[o + t] += x[t];
+      a.total[o + t] = a.base[o + t] + a.delta[o + t];
+    }
+    if (bad) atomicOr(a.flags + pair, kFlagStep);
+  }
+  cl.sync();  // no CTA leaves while a partner may still read its shared partials
+}
+
 }  // namespace
 
 void init_solve_attributes() {
@@ -589,7 +724,16 @@ void launch_schwarz(const SwzArgs& a_in, int B, cudaStream_t s) {
 }
 
 void launch_pcg_global(const PcgArgs& a, int B, cudaStream_t s) {
-  k_pcg_global<<<B, kPcgThreads, 0, s>>>(a);
+  static const int sms = [] {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  if (B < sms)  // fewer pairs than SMs: a cluster of CTAs per pair
+    k_pcg_cluster<<<B * kPcgCluster, kPcgClusterThreads, 0, s>>>(a);
+  else
+    k_pcg_global<<<B, kPcgThreads, 0, s>>>(a);
 }
 
 }  // namespace hwf
