@@ -52,6 +52,7 @@ def extra_configs(dev, lib, h, C, capi, reps: int = 5) -> dict:
     """The other BASELINE.json shapes on this GPU, device-resident replays (not the headline):
     cfg3 1920x1080 occluder + illumination change, 5 levels, 8 px grid, batch 4;
     cfg5 3840x2160 single frame pair, 5 levels, 4 px grid (north_star: >= 30 Hz);
+    cfg1 (BASELINE configs[0]) 320x240, 3 levels, fixed 5 GN x 10 PCG in global mode, batch 128;
     SURVEY §8f rank 3 at cfg2 scale, batch 32: stereo-only (active_fields = s, global PCG; the
     reference's Schwarz mode hits pAp <= 0 on it) and the stereo-hq preset with the epipolar term on
     (w_epi = 0.5, rectified-rig F)."""
@@ -63,6 +64,10 @@ def extra_configs(dev, lib, h, C, capi, reps: int = 5) -> dict:
               SolveSchedule(levels=5, grid_step=8, pcg_iters=5, patch_iters=5), EnergyParams(), None),
              ("cfg5_3840x2160_single_frame", lambda: synthetic.uhd_pair(0)[0][None],
               SolveSchedule(levels=5, grid_step=4, pcg_iters=5, patch_iters=5), EnergyParams(), None),
+             ("cfg1_320x240_5gn_10pcg_global_batch128",
+              lambda: np.stack([synthetic.constant_pair(320, 240, seed=1610 + i)[0] for i in range(128)]),
+              SolveSchedule(levels=3, grid_step=8, gn_per_level=[5, 5, 5], pcg_iters=10, subdomain_px=0),
+              EnergyParams(), None),
              ("cfg2_stereo_only_global_pcg_batch32", lambda: make_frames(32, 0),
               SolveSchedule(levels=4, grid_step=8, pcg_iters=5, subdomain_px=0, active_fields=1), EnergyParams(),
               None),
