@@ -491,27 +491,36 @@ __global__ void k_dense(int w, int h, int gw, int gh, int step, const double* __
 }
 
 // ---- energy partials -> per (pair, slot) breakdown, fixed order -----------
-// Warp per (pair, slot): lane l sums partials l, l+32, ... in order, then a
-// fixed xor tree — deterministic and independent of scheduling.
-__global__ void k_energy_reduce(const double* __restrict__ ep, int nslots, int cap, int B, double* out, int* flags) {
-  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (t >= B * nslots) return;
+// CTA per (pair, slot): thread t sums partials t, t + 256, ... in order, then fixed xor trees within
+// the warps and warp 0 over the 8 warp sums: deterministic and independent of scheduling. (A single
+// warp per slot took 2.5 ms at 4K, where a slot holds ~160k partials.)
+constexpr int kReduceThreads = 256;
+__global__ void __launch_bounds__(kReduceThreads) k_energy_reduce(const double* __restrict__ ep, int nslots, int cap,
+                                                                  int B, double* out, int* flags) {
+  __shared__ double red[kReduceThreads / 32][kNumEnergy];
+  const int t = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int pair = t / nslots;
   const double* p = ep + static_cast<size_t>(t) * cap * kNumEnergy;
   double s[kNumEnergy] = {0, 0, 0, 0, 0};
-  for (int i = lane; i < cap; i += 32)
+  for (int i = threadIdx.x; i < cap; i += kReduceThreads)
 #pragma unroll
     for (int k = 0; k < kNumEnergy; ++k) s[k] += p[i * kNumEnergy + k];
-  bool bad = false;
 #pragma unroll
-  for (int k = 0; k < kNumEnergy; ++k) {
-    s[k] = warp_sum(s[k]);
-    bad = bad || !isfinite(s[k]);
-  }
-  if (lane == 0) {
+  for (int k = 0; k < kNumEnergy; ++k) s[k] = warp_sum(s[k]);
+  if (lane == 0)
 #pragma unroll
-    for (int k = 0; k < kNumEnergy; ++k) out[static_cast<size_t>(t) * kNumEnergy + k] = s[k];
-    if (bad) atomicOr(flags + pair, kFlagEnergy);
+    for (int k = 0; k < kNumEnergy; ++k) red[warp][k] = s[k];
+  __syncthreads();
+  if (warp == 0) {
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < kNumEnergy; ++k) {
+      double v = lane < kReduceThreads / 32 ? red[lane][k] : 0.0;
+      v = warp_sum(v);
+      bad = bad || !isfinite(v);
+      if (lane == 0) out[static_cast<size_t>(t) * kNumEnergy + k] = v;
+    }
+    if (lane == 0 && bad) atomicOr(flags + pair, kFlagEnergy);
   }
 }
 
@@ -592,8 +601,7 @@ void launch_dense(int w, int h, int gw, int gh, int step, const double* total, i
   k_dense<<<rows_grid(w, h, B), kThreads, 0, s>>>(w, h, gw, gh, step, total, s_out, m_out, d_out, disp_out);
 }
 void launch_energy_reduce(const double* ep, int nslots, int cap, int B, double* out, int* flags, cudaStream_t s) {
-  const long long n = 32LL * nslots * B;
-  k_energy_reduce<<<static_cast<unsigned>((n + kThreads - 1) / kThreads), kThreads, 0, s>>>(ep, nslots, cap, B, out, flags);
+  k_energy_reduce<<<static_cast<unsigned>(nslots * B), kReduceThreads, 0, s>>>(ep, nslots, cap, B, out, flags);
 }
 
 }  // namespace hwf
