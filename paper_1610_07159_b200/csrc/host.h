@@ -131,8 +131,10 @@ struct Scratch {  // shared across levels, sized for the finest
   unsigned long long* queue = nullptr;  // large-triangle raster queue (every triangle, worst case)
   unsigned int* qcount = nullptr;
   double *resid = nullptr, *tmp = nullptr;
-  double *px = nullptr, *pr = nullptr, *pz = nullptr, *pp = nullptr, *pap = nullptr;
-  void alloc(DevMem& m, int B, size_t N, size_t G, bool occ, bool illum, bool pcg) {
+  double *px = nullptr, *pr = nullptr, *pz = nullptr, *pp = nullptr, *pap = nullptr, *pp2 = nullptr;
+  double *ppart = nullptr, *pstate = nullptr;
+  unsigned* pcount = nullptr;
+  void alloc(DevMem& m, int B, size_t N, size_t G, bool occ, bool illum, bool pcg, int pcg_tiles_max = 0) {
     if (occ) {
       q = m.alloc<int2>(B * N * 4);
       Z = m.alloc<float>(B * N);
@@ -152,6 +154,11 @@ struct Scratch {  // shared across levels, sized for the finest
       pz = m.alloc<double>(B * G * 6);
       pp = m.alloc<double>(B * G * 6);
       pap = m.alloc<double>(B * G * 6);
+      pp2 = m.alloc<double>(B * G * 6);
+      ppart = m.alloc<double>(static_cast<size_t>(B) * pcg_tiles_max * 2);
+      pstate = m.alloc<double>(static_cast<size_t>(B) * 8);
+      pcount = m.alloc<unsigned>(B);
+      CK(cudaMemset(pcount, 0, B * sizeof(unsigned)));
     }
   }
 };
@@ -210,6 +217,7 @@ inline NodeArgs node_args(const LevelDev& d, const hwf_energy_params& P, const h
   na.half = d.half; na.node_w = d.nodew; na.node_w_new = d.nodew; na.total = d.total; na.delta = d.delta;
   na.cells = d.cells; na.sys = d.sys; na.ep_pair = E.pair_stride(); na.ep_base = d.n_pix_cta; na.flags = flags;
   na.P = to_params(P); na.F = dF; na.active = S.active_fields; na.lm = S.lm_lambda;
+  na.soa = S.subdomain_px <= 0;  // the global PCG reads entry-major records
   if (R && !R->whole) {
     na.n_lo = R->n_lo; na.n_hi = R->n_hi; na.own_lo = R->own_lo; na.own_hi = R->own_hi;
   }
@@ -302,10 +310,11 @@ inline void record_gn_level(LevelDev& d, int B, const hwf_energy_params& P, cons
       PcgArgs ga{};
       ga.gw = d.gw; ga.gh = d.gh; ga.iters = S.pcg_iters; ga.sys = d.sys;
       ga.x = sc.px; ga.r = sc.pr; ga.z = sc.pz; ga.p = sc.pp; ga.ap = sc.pap; ga.update = 1;
+      ga.p2 = sc.pp2; ga.part = sc.ppart; ga.state = sc.pstate; ga.count = sc.pcount;
       ga.trace = pcg_trace ? pcg_trace + static_cast<size_t>(it) * (S.pcg_iters + 1) : nullptr;
       ga.delta = d.delta; ga.total = d.total; ga.base = d.base; ga.active = S.active_fields; ga.flags = flags;
       launch_pcg_global(ga, B, st);
-      L.count += 1;
+      L.count += pcg_launches(S.pcg_iters);
     }
   }
   if (gn > 0 && energy_after) rec_energy_after(d, B, P, S, dF, gn, E, slot_base, flags, st, L, src8);
@@ -480,7 +489,7 @@ struct Plan {
         lv[l - 1].hc = d.h;
       }
     }
-    sc.alloc(mem, B, N0, lv[0].G, true, L > 1, S.subdomain_px <= 0);
+    sc.alloc(mem, B, N0, lv[0].G, true, L > 1, S.subdomain_px <= 0, pcg_tiles(lv[0].gw, lv[0].gh));
     E.nslots = std::max(nslots, 1);
     E.cap = static_cast<int>(cap);
     E.part = mem.alloc<double>(static_cast<size_t>(B) * E.pair_stride());

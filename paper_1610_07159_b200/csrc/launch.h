@@ -53,7 +53,8 @@ struct NodeArgs {
   const double* total;  // [B][G][6]
   const double* delta;  // [B][G][6]
   const double* cells;  // [B][C][234]
-  double* sys;          // [B][G][120]
+  double* sys;          // [B][G][120], or [B][120][G] when soa (global PCG mode)
+  int soa;
   double* ep_new;
   double* ep_old;
   long long ep_pair;
@@ -90,6 +91,10 @@ struct PcgArgs {
   int gw, gh, iters;
   const double* sys;
   double *x, *r, *z, *p, *ap;  // [B][6G] scratch
+  double* p2;                  // [B][6G] second search-direction buffer (p ping-pongs)
+  double* part;                // [B][pcg_tiles][2] per-tile dot partials
+  double* state;               // [B][8] rz, rz0, alpha, beta, stop between kernels
+  unsigned* count;             // [B] last-CTA counters, zero between launches
   double* trace;               // [B][iters+1] or null
   int update;                  // apply delta += x, total = base + delta
   double* delta;
@@ -118,6 +123,8 @@ void launch_structw(int w, int h, int gw, int gh, int step, const double* half, 
 
 // solve.cu
 void launch_schwarz(const SwzArgs& a, int B, cudaStream_t s);
+int pcg_tiles(int gw, int gh);  // tiles of one level (PcgArgs::part rows)
+int pcg_launches(int iters);
 void launch_pcg_global(const PcgArgs& a, int B, cudaStream_t s);
 
 // maps.cu

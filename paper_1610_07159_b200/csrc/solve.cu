@@ -11,17 +11,14 @@
 // warp sums (deterministic, identical in every lane). The last sweep fuses the
 // Gauss-Newton update delta += step, total = base + delta (solver.cpp:518-523).
 //
-// k_pcg_global: the subdomain_px = 0 mode (pcg_solve, solver.cpp:365-380), one
-// CTA per frame pair looping over all iterations with block-wide fixed-order dots.
+// k_pcg_init / k_pcg_spmv / k_pcg_update: the subdomain_px = 0 mode (pcg_solve,
+// solver.cpp:365-380), tiled over the whole GPU with fixed-order dots (see below).
 #include <algorithm>
 #include <cstdlib>
-
-#include <cooperative_groups.h>
 
 #include "launch.h"
 
 namespace hwf {
-namespace cg = cooperative_groups;
 namespace {
 
 // Row r of block(n, slot9) of the symmetric system.
@@ -431,255 +428,320 @@ __global__ void __launch_bounds__(128) k_schwarz22(const SwzArgs a, int nsub, in
   }
 }
 
-constexpr int kPcgThreads = 1024;
+// ---- global PCG (subdomain_px = 0; pcg_solve, solver.cpp:365-380; pcg_impl, :320-361) ---------------
+// Three kernels, each spread over (tiles, pairs):
+//   k_pcg_init    x = 0, r = b, z = M r, p = 0                              partials r.z, r.r
+//   k_pcg_spmv    p = z + beta p (tile and halo, staged in shared memory), Ap   partial p.Ap
+//   k_pcg_update  x += alpha p, r -= alpha Ap, z = M r                     partials r.z, r.r
+// A tile is a segment of 32 nodes of one grid row, one warp, one node per lane. The system is
+// entry-major ([entry][node], written so by k_node in this mode), so a lane's 21 loads of a block
+// are 256 B coalesced rows across the warp. Every dot is the same fixed tree: per node
+// ((u0v0 + u1v1) + (u2v2 + u3v3)) + (u4v4 + u5v5) rounded op by op, an xor tree over the 32 lanes,
+// then the pair's tiles in index order (strided over 128 threads, xor trees, the 4 warps in order),
+// summed by whichever CTA of the pair finishes last. The order depends only on the level's tiling:
+// results are bitwise independent of the batch size. The per-pair scalars (rz, alpha, beta, a
+// stop bit) live in `state` between kernels; a pair that meets a divergence condition stops
+// iterating (flag set) and still applies its step at the end.
+constexpr int kPcgTile = 32, kPcgWarps = 4, kPcgThreads = 32 * kPcgWarps;
+enum : int { kStRz = 0, kStRz0, kStAlpha, kStBeta, kStStop, kStCount = 8 };
 
-__device__ double block_dot(const double* __restrict__ x, const double* __restrict__ y, int n, double* red) {
+struct PcgTile {
+  int b, a0, width, tile, ntiles, nctas;
+  bool live;
+};
+__device__ __forceinline__ PcgTile pcg_tile(int gw, int gh) {
+  const int tpr = (gw + kPcgTile - 1) / kPcgTile;
+  PcgTile T;
+  T.ntiles = tpr * gh;
+  T.nctas = (T.ntiles + kPcgWarps - 1) / kPcgWarps;
+  T.tile = blockIdx.x * kPcgWarps + (threadIdx.x >> 5);
+  T.live = T.tile < T.ntiles;
+  const int t = T.live ? T.tile : T.ntiles - 1;
+  T.b = t / tpr;
+  T.a0 = (t - T.b * tpr) * kPcgTile;
+  T.width = T.live ? min(kPcgTile, gw - T.a0) : 0;
+  return T;
+}
+
+__device__ __forceinline__ double node_dot(const double (&u)[6], const double (&v)[6]) {
+  const double s01 = __dadd_rn(__dmul_rn(u[0], v[0]), __dmul_rn(u[1], v[1]));
+  const double s23 = __dadd_rn(__dmul_rn(u[2], v[2]), __dmul_rn(u[3], v[3]));
+  const double s45 = __dadd_rn(__dmul_rn(u[4], v[4]), __dmul_rn(u[5], v[5]));
+  return __dadd_rn(__dadd_rn(s01, s23), s45);
+}
+
+// Sum of the pair's tile partials part[k * stride], k < n, in the canonical order; every thread
+// of the CTA returns the same value.
+__device__ __forceinline__ double pair_total(const double* part, int n, int stride, double* red) {
   double s = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) s += x[i] * y[i];
+  for (int k = threadIdx.x; k < n; k += kPcgThreads) s += __ldcg(part + static_cast<size_t>(k) * stride);
   s = warp_sum(s);
   __syncthreads();
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
   __syncthreads();
-  double t = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
-  if (threadIdx.x < 32) t = warp_sum(t);
-  __syncthreads();
-  if (threadIdx.x == 0) red[32] = t;
-  __syncthreads();
-  return red[32];
+  double t = 0.0;
+#pragma unroll
+  for (int w = 0; w < kPcgWarps; ++w) t += red[w];
+  return t;
 }
 
-__device__ void spmv(const double* __restrict__ sys, int gw, int gh, const double* __restrict__ x,
-                     double* __restrict__ y) {
-  const int G = gw * gh;
-  for (int t = threadIdx.x; t < 6 * G; t += blockDim.x) {
-    const int n = t / 6, r = t % 6, na = n % gw, nb = n / gw;
-    double acc = 0.0;
-    for (int s9 = 0; s9 < 9; ++s9) {
-      const int qa = na + s9 % 3 - 1, qb = nb + s9 / 3 - 1;
-      if (qa < 0 || qa >= gw || qb < 0 || qb >= gh) continue;
-      const int qn = qb * gw + qa;
-      for (int c = 0; c < 6; ++c) acc += sys_entry(sys, G, n, qn, s9, r, c) * x[6 * qn + c];
+// Publishes this CTA's partials and reports whether it is the pair's last CTA to do so.
+__device__ __forceinline__ bool pcg_last_cta(unsigned* count, int nctas, int* sflag) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) *sflag = atomicAdd(count, 1u) == static_cast<unsigned>(nctas - 1);
+  __syncthreads();
+  const bool last = *sflag != 0;
+  if (last) {
+    __threadfence();
+    if (threadIdx.x == 0) *count = 0;  // ready for the next kernel
+  }
+  return last;
+}
+
+struct PcgPtr {
+  const double* sys;  // entry-major: entry e of node n at sys[e * G + n]
+  double *x, *r, *z, *ap, *part, *st;
+  unsigned* cnt;
+  double* tr;
+  size_t G;
+};
+__device__ __forceinline__ PcgPtr pcg_ptr(const PcgArgs& a, int ntiles) {
+  const int pair = blockIdx.y;
+  const size_t G = static_cast<size_t>(a.gw) * a.gh, M = 6 * G;
+  PcgPtr P;
+  P.G = G;
+  P.sys = a.sys + pair * G * kSysStride;
+  P.x = a.x + pair * M;
+  P.r = a.r + pair * M;
+  P.z = a.z + pair * M;
+  P.ap = a.ap + pair * M;
+  P.part = a.part + static_cast<size_t>(pair) * ntiles * 2;
+  P.st = a.state + static_cast<size_t>(pair) * kStCount;
+  P.cnt = a.count + pair;
+  P.tr = a.trace ? a.trace + static_cast<size_t>(pair) * (a.iters + 1) : nullptr;
+  return P;
+}
+
+__device__ __forceinline__ void ld6(const double* p, double (&v)[6]) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const double2 t = __ldcg(q + i);
+    v[2 * i] = t.x;
+    v[2 * i + 1] = t.y;
+  }
+}
+__device__ __forceinline__ void st6(double* p, const double (&v)[6]) {
+  double2* q = reinterpret_cast<double2*>(p);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) q[i] = make_double2(v[2 * i], v[2 * i + 1]);
+}
+
+// z = M r (solver.cpp:468-474 via NormalSystem::precond_block): the node's three 2x2 blocks
+__device__ __forceinline__ void pcg_precond(const PcgPtr& P, size_t n, const double (&r)[6], double (&z)[6]) {
+#pragma unroll
+  for (int f = 0; f < 3; ++f) {
+    const double m0 = __ldg(P.sys + (kSysPre + 3 * f) * P.G + n);
+    const double m1 = __ldg(P.sys + (kSysPre + 3 * f + 1) * P.G + n);
+    const double m2 = __ldg(P.sys + (kSysPre + 3 * f + 2) * P.G + n);
+    z[2 * f] = m0 * r[2 * f] + m1 * r[2 * f + 1];
+    z[2 * f + 1] = m1 * r[2 * f] + m2 * r[2 * f + 1];
+  }
+}
+
+// Tile partial of one per-node value (xor tree over the warp); every lane returns it.
+__device__ __forceinline__ double tile_partial(bool act, double v) { return warp_sum(act ? v : 0.0); }
+
+__device__ __forceinline__ void pcg_apply_step(const PcgArgs& a, const PcgPtr& P, size_t n, bool act) {
+  bool bad = false;
+  if (act) {
+    const size_t o = static_cast<size_t>(blockIdx.y) * 6 * P.G + 6 * n;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      const double xv = P.x[6 * n + k];
+      bad = bad || !isfinite(xv);
+      if ((a.active >> (k >> 1)) & 1) a.delta[o + k] += xv;
+      a.total[o + k] = a.base[o + k] + a.delta[o + k];
     }
-    y[t] = acc;
   }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(a.flags + blockIdx.y, kFlagStep);
 }
 
-__device__ void precondition(const double* __restrict__ sys, int G, const double* __restrict__ r,
-                             double* __restrict__ z) {
-  for (int t = threadIdx.x; t < 6 * G; t += blockDim.x) {
-    const int n = t / 6, k = t % 6;
-    const double* pre = sys + static_cast<size_t>(n) * kSysStride + kSysPre + 3 * (k >> 1);
-    const int e = t & ~1;
-    z[t] = (k & 1) ? pre[1] * r[e] + pre[2] * r[e + 1] : pre[0] * r[e] + pre[1] * r[e + 1];
+__global__ void __launch_bounds__(kPcgThreads) k_pcg_init(const PcgArgs a) {
+  __shared__ double red[kPcgWarps];
+  __shared__ int sflag;
+  const PcgTile T = pcg_tile(a.gw, a.gh);
+  const PcgPtr P = pcg_ptr(a, T.ntiles);
+  const int j = threadIdx.x & 31;
+  const bool act = j < T.width;
+  const size_t n = static_cast<size_t>(T.b) * a.gw + T.a0 + min(j, max(T.width - 1, 0));
+  double r[6], z[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) r[k] = act ? __ldg(P.sys + (kSysRhs + k) * P.G + n) : 0.0;
+  pcg_precond(P, n, r, z);
+  if (act) {
+    const double zero[6] = {0, 0, 0, 0, 0, 0};
+    st6(P.x + 6 * n, zero);
+    st6(P.r + 6 * n, r);
+    st6(P.z + 6 * n, z);
+    st6(a.p + static_cast<size_t>(blockIdx.y) * 6 * P.G + 6 * n, zero);
   }
-}
-
-__global__ void __launch_bounds__(kPcgThreads) k_pcg_global(const PcgArgs a) {
-  __shared__ double red[33];
-  const int pair = blockIdx.x;
-  const int G = a.gw * a.gh, M = 6 * G;
-  const double* sys = a.sys + static_cast<size_t>(pair) * G * kSysStride;
-  double* x = a.x + static_cast<size_t>(pair) * M;
-  double* r = a.r + static_cast<size_t>(pair) * M;
-  double* z = a.z + static_cast<size_t>(pair) * M;
-  double* p = a.p + static_cast<size_t>(pair) * M;
-  double* ap = a.ap + static_cast<size_t>(pair) * M;
-  double* tr = a.trace ? a.trace + static_cast<size_t>(pair) * (a.iters + 1) : nullptr;
-  for (int t = threadIdx.x; t < M; t += blockDim.x) {
-    x[t] = 0.0;
-    r[t] = __ldg(sys + static_cast<size_t>(t / 6) * kSysStride + kSysRhs + t % 6);
+  const double prz = tile_partial(act, node_dot(r, z));
+  const double prr = tile_partial(act, node_dot(r, r));
+  if (j == 0 && T.live) {
+    P.part[2 * T.tile] = prz;
+    P.part[2 * T.tile + 1] = prr;
   }
-  __syncthreads();
-  if (tr) {
-    const double nr = block_dot(r, r, M, red);
-    if (threadIdx.x == 0) tr[0] = sqrt(nr);
+  if (pcg_last_cta(P.cnt, T.nctas, &sflag)) {
+    const double rz = pair_total(P.part, T.ntiles, 2, red);
+    const double rr = pair_total(P.part + 1, T.ntiles, 2, red);
+    if (threadIdx.x == 0) {
+      if (P.tr) P.tr[0] = sqrt(rr);
+      P.st[kStRz] = rz;
+      P.st[kStRz0] = fabs(rz);
+      P.st[kStBeta] = 0.0;
+      P.st[kStStop] = rz == 0.0 ? 1.0 : 0.0;  // early return (solver.cpp:334-338)
+      if (rz == 0.0 && P.tr)
+        for (int it = 0; it < a.iters; ++it) P.tr[it + 1] = 0.0;
+    }
   }
-  precondition(sys, G, r, z);
-  __syncthreads();
-  double rz = block_dot(r, z, M, red);
-  const double rz0 = fabs(rz);
-  int flag = 0;
-  if (rz0 == 0.0) {
-    if (tr && threadIdx.x == 0)
-      for (int it = 0; it < a.iters; ++it) tr[it + 1] = 0.0;
-  } else {
-    for (int t = threadIdx.x; t < M; t += blockDim.x) p[t] = z[t];
+  if (a.iters == 0 && a.update) {
     __syncthreads();
-    for (int it = 0; it < a.iters; ++it) {
-      spmv(sys, a.gw, a.gh, p, ap);
-      __syncthreads();
-      const double pAp = block_dot(p, ap, M, red);
-      if (pAp <= 0.0) {
-        flag = kFlagCurvature;
-        break;
-      }
-      const double alpha = rz / pAp;
-      for (int t = threadIdx.x; t < M; t += blockDim.x) {
-        x[t] += alpha * p[t];
-        r[t] -= alpha * ap[t];
-      }
-      __syncthreads();
-      if (tr) {
-        const double nr = block_dot(r, r, M, red);
-        if (threadIdx.x == 0) tr[it + 1] = sqrt(nr);
-      }
-      precondition(sys, G, r, z);
-      __syncthreads();
-      const double rzn = block_dot(r, z, M, red);
-      if (fabs(rzn) > 100.0 * rz0) {
-        flag = kFlagGrowth;
-        break;
-      }
-      const double beta = rzn / rz;
-      rz = rzn;
-      for (int t = threadIdx.x; t < M; t += blockDim.x) p[t] = z[t] + beta * p[t];
-      __syncthreads();
-    }
-  }
-  if (flag && threadIdx.x == 0) atomicOr(a.flags + pair, flag);
-  __syncthreads();
-  if (a.update) {
-    const size_t o = static_cast<size_t>(pair) * M;
-    bool bad = false;
-    for (int t = threadIdx.x; t < M; t += blockDim.x) {
-      bad = bad || !isfinite(x[t]);
-      if ((a.active >> ((t % 6) >> 1)) & 1) a.delta[o + t] += x[t];
-      a.total[o + t] = a.base[o + t] + a.delta[o + t];
-    }
-    if (bad) atomicOr(a.flags + pair, kFlagStep);
+    pcg_apply_step(a, P, n, act);
   }
 }
 
-// ---- k_pcg_cluster: the same global PCG with a thread-block cluster per pair -------------------------
-// k_pcg_global runs one CTA per pair, so a batch smaller than the SM count leaves most of the GPU idle.
-// Here a cluster of kPcgCluster CTAs shares one pair. Each CTA owns a contiguous node slice of every
-// vector. Dots reduce per CTA in a fixed order, then every CTA sums the kPcgCluster partials in rank
-// order through distributed shared memory, so all CTAs hold the same bits. Cluster barriers
-// (release/acquire) make each CTA's slice of p visible to the others' SpMV.
-constexpr int kPcgCluster = 8, kPcgClusterThreads = 256;
-
-__device__ double slice_dot(const double* __restrict__ x, const double* __restrict__ y, int lo, int hi, double* red,
-                            double* part, cg::cluster_group& cl) {
-  double s = 0.0;
-  for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) s += x[i] * y[i];
-  s = warp_sum(s);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
-    *part = t;
+// p_next = z + beta p_prev over the tile and its one-node halo (per-warp shared memory, field-major
+// so lane j reads consecutive words), Ap = A p_next with the 9-slot block SpMV.
+constexpr int kPhCols = kPcgTile + 4;
+__global__ void __launch_bounds__(kPcgThreads) k_pcg_spmv(const PcgArgs a, const double* __restrict__ p_prev,
+                                                         double* __restrict__ p_next) {
+  __shared__ double ph_all[kPcgWarps][3][6][kPhCols];
+  __shared__ double red[kPcgWarps];
+  __shared__ int sflag;
+  const PcgTile T = pcg_tile(a.gw, a.gh);
+  const PcgPtr P = pcg_ptr(a, T.ntiles);
+  if (__ldcg(P.st + kStStop) != 0.0) return;
+  const double beta = __ldcg(P.st + kStBeta);
+  const size_t op = static_cast<size_t>(blockIdx.y) * 6 * P.G;
+  const int j = threadIdx.x & 31;
+  double (*ph)[6][kPhCols] = ph_all[threadIdx.x >> 5];
+  // rows b-1..b+1, nodes a0-1 .. a0+width: 6 (width + 2) contiguous doubles per row
+  const int span = 6 * (T.width + 2);
+  for (int row = 0; row < 3; ++row) {
+    const int qb = T.b - 1 + row;
+    for (int i = j; i < span; i += 32) {
+      const int col = i / 6, c = i - 6 * col, qa = T.a0 - 1 + col;
+      double v = 0.0;
+      if (qa >= 0 && qa < a.gw && qb >= 0 && qb < a.gh) {
+        const size_t o = 6 * (static_cast<size_t>(qb) * a.gw + qa) + c;
+        v = __ldcg(P.z + o) + beta * __ldcg(p_prev + op + o);  // p = z + beta p (solver.cpp:358)
+        if (row == 1 && col >= 1 && col <= T.width) p_next[op + o] = v;
+      }
+      ph[row][c][col] = v;
+    }
   }
-  cl.sync();
-  double tot = 0.0;
-  for (int k = 0; k < kPcgCluster; ++k) tot += *cl.map_shared_rank(part, k);
-  return tot;
+  __syncwarp();
+  const bool act = j < T.width;
+  const int a_ = T.a0 + min(j, max(T.width - 1, 0));
+  const size_t n = static_cast<size_t>(T.b) * a.gw + a_;
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+#pragma unroll
+  for (int s9 = 0; s9 < 9; ++s9) {  // NormalSystem::apply (solver.cpp:80-98)
+    const int dx = s9 % 3 - 1, dy = s9 / 3 - 1;
+    const int qa = a_ + dx, qb = T.b + dy;
+    const bool valid = act && qa >= 0 && qa < a.gw && qb >= 0 && qb < a.gh;
+    if (!valid) continue;
+    // forward slots from this node's record, backward ones as the neighbour's forward block
+    const size_t nq = s9 >= 4 ? n : static_cast<size_t>(qb) * a.gw + qa;
+    const double* blk = P.sys + static_cast<size_t>(s9 >= 4 ? s9 - 4 : 4 - s9) * 21 * P.G + nq;
+    double A[21];
+#pragma unroll
+    for (int m = 0; m < 21; ++m) A[m] = __ldg(blk + m * P.G);
+    double pv[6];
+#pragma unroll
+    for (int c = 0; c < 6; ++c) pv[c] = ph[1 + dy][c][j + 1 + dx];
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+      for (int c = 0; c < 6; ++c) acc[i] += A[sym6(i, c)] * pv[c];
+  }
+  double pown[6];
+#pragma unroll
+  for (int c = 0; c < 6; ++c) pown[c] = ph[1][c][j + 1];
+  if (act) st6(P.ap + 6 * n, acc);
+  const double part = tile_partial(act, node_dot(pown, acc));
+  if (j == 0 && T.live) P.part[2 * T.tile] = part;
+  if (pcg_last_cta(P.cnt, T.nctas, &sflag)) {
+    const double pAp = pair_total(P.part, T.ntiles, 2, red);
+    if (threadIdx.x == 0) {
+      if (pAp <= 0.0) {  // solver.cpp:344-346
+        P.st[kStStop] = 1.0;
+        atomicOr(a.flags + blockIdx.y, kFlagCurvature);
+      } else {
+        P.st[kStAlpha] = P.st[kStRz] / pAp;
+      }
+    }
+  }
 }
 
-__global__ void __cluster_dims__(kPcgCluster, 1, 1) __launch_bounds__(kPcgClusterThreads)
-    k_pcg_cluster(const PcgArgs a) {
-  __shared__ double red[kPcgClusterThreads / 32];
-  __shared__ double part[2];  // alternating dot partials (a partial is rewritten two dots later)
-  cg::cluster_group cl = cg::this_cluster();
-  const int rank = static_cast<int>(cl.block_rank());
-  const int pair = blockIdx.x / kPcgCluster;
-  const int G = a.gw * a.gh, M = 6 * G;
-  const int lo = 6 * static_cast<int>(static_cast<long long>(G) * rank / kPcgCluster);
-  const int hi = 6 * static_cast<int>(static_cast<long long>(G) * (rank + 1) / kPcgCluster);
-  const double* sys = a.sys + static_cast<size_t>(pair) * G * kSysStride;
-  double* x = a.x + static_cast<size_t>(pair) * M;
-  double* r = a.r + static_cast<size_t>(pair) * M;
-  double* z = a.z + static_cast<size_t>(pair) * M;
-  double* p = a.p + static_cast<size_t>(pair) * M;
-  double* ap = a.ap + static_cast<size_t>(pair) * M;
-  double* tr = a.trace ? a.trace + static_cast<size_t>(pair) * (a.iters + 1) : nullptr;
-  int nd = 0;  // dots issued (selects the partial slot)
-  auto dot = [&](const double* u, const double* v) { return slice_dot(u, v, lo, hi, red, &part[nd++ & 1], cl); };
-  auto spmv_slice = [&](const double* xv, double* y) {  // rows [lo, hi) of the 9-slot block SpMV
-    for (int t = lo + threadIdx.x; t < hi; t += blockDim.x) {
-      const int n = t / 6, rr = t % 6, na = n % a.gw, nb = n / a.gw;
-      double acc = 0.0;
-      for (int s9 = 0; s9 < 9; ++s9) {
-        const int qa = na + s9 % 3 - 1, qb = nb + s9 / 3 - 1;
-        if (qa < 0 || qa >= a.gw || qb < 0 || qb >= a.gh) continue;
-        const int qn = qb * a.gw + qa;
-        for (int c = 0; c < 6; ++c) acc += sys_entry(sys, G, n, qn, s9, rr, c) * xv[6 * qn + c];
-      }
-      y[t] = acc;
-    }
-  };
-  auto precond_slice = [&]() {
-    for (int t = lo + threadIdx.x; t < hi; t += blockDim.x) {
-      const int n = t / 6, k = t % 6;
-      const double* pre = sys + static_cast<size_t>(n) * kSysStride + kSysPre + 3 * (k >> 1);
-      const int e = t & ~1;
-      z[t] = (k & 1) ? pre[1] * r[e] + pre[2] * r[e + 1] : pre[0] * r[e] + pre[1] * r[e + 1];
-    }
-  };
-  for (int t = lo + threadIdx.x; t < hi; t += blockDim.x) {
-    x[t] = 0.0;
-    r[t] = __ldg(sys + static_cast<size_t>(t / 6) * kSysStride + kSysRhs + t % 6);
+__global__ void __launch_bounds__(kPcgThreads) k_pcg_update(const PcgArgs a, const double* __restrict__ p_cur,
+                                                           int it) {
+  __shared__ double red[kPcgWarps];
+  __shared__ int sflag;
+  const PcgTile T = pcg_tile(a.gw, a.gh);
+  const PcgPtr P = pcg_ptr(a, T.ntiles);
+  const int j = threadIdx.x & 31;
+  const bool act = j < T.width;
+  const size_t n = static_cast<size_t>(T.b) * a.gw + T.a0 + min(j, max(T.width - 1, 0));
+  const bool final_step = a.update && it == a.iters - 1;
+  if (__ldcg(P.st + kStStop) != 0.0) {
+    if (final_step) pcg_apply_step(a, P, n, act);
+    return;
   }
-  __syncthreads();
-  if (tr) {
-    const double nr = dot(r, r);
-    if (rank == 0 && threadIdx.x == 0) tr[0] = sqrt(nr);
+  const double alpha = __ldcg(P.st + kStAlpha);
+  double r[6] = {0, 0, 0, 0, 0, 0}, z[6];
+  if (act) {
+    double x[6], p[6], ap[6];
+    ld6(P.x + 6 * n, x);
+    ld6(p_cur + static_cast<size_t>(blockIdx.y) * 6 * P.G + 6 * n, p);
+    ld6(P.r + 6 * n, r);
+    ld6(P.ap + 6 * n, ap);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      x[k] += alpha * p[k];  // solver.cpp:348-349
+      r[k] -= alpha * ap[k];
+    }
+    st6(P.x + 6 * n, x);
+    st6(P.r + 6 * n, r);
   }
-  precond_slice();
-  __syncthreads();
-  double rz = dot(r, z);
-  const double rz0 = fabs(rz);
-  int flag = 0;
-  if (rz0 == 0.0) {
-    if (tr && rank == 0 && threadIdx.x == 0)
-      for (int it = 0; it < a.iters; ++it) tr[it + 1] = 0.0;
-  } else {
-    for (int t = lo + threadIdx.x; t < hi; t += blockDim.x) p[t] = z[t];
-    cl.sync();  // every slice of p is written before any SpMV reads it
-    for (int it = 0; it < a.iters; ++it) {
-      spmv_slice(p, ap);
-      __syncthreads();
-      const double pAp = dot(p, ap);
-      if (pAp <= 0.0) {
-        flag = kFlagCurvature;
-        break;
+  pcg_precond(P, n, r, z);
+  if (act) st6(P.z + 6 * n, z);
+  const double prz = tile_partial(act, node_dot(r, z));
+  const double prr = P.tr ? tile_partial(act, node_dot(r, r)) : 0.0;
+  if (j == 0 && T.live) {
+    P.part[2 * T.tile] = prz;
+    P.part[2 * T.tile + 1] = prr;
+  }
+  if (pcg_last_cta(P.cnt, T.nctas, &sflag)) {
+    const double rzn = pair_total(P.part, T.ntiles, 2, red);
+    const double rr = P.tr ? pair_total(P.part + 1, T.ntiles, 2, red) : 0.0;
+    if (threadIdx.x == 0) {
+      if (P.tr) P.tr[it + 1] = sqrt(rr);
+      if (fabs(rzn) > 100.0 * P.st[kStRz0]) {  // solver.cpp:352-355
+        P.st[kStStop] = 1.0;
+        atomicOr(a.flags + blockIdx.y, kFlagGrowth);
+      } else {
+        P.st[kStBeta] = rzn / P.st[kStRz];
+        P.st[kStRz] = rzn;
       }
-      const double alpha = rz / pAp;
-      for (int t = lo + threadIdx.x; t < hi; t += blockDim.x) {
-        x[t] += alpha * p[t];
-        r[t] -= alpha * ap[t];
-      }
-      __syncthreads();
-      if (tr) {
-        const double nr = dot(r, r);
-        if (rank == 0 && threadIdx.x == 0) tr[it + 1] = sqrt(nr);
-      }
-      precond_slice();
-      __syncthreads();
-      const double rzn = dot(r, z);
-      if (fabs(rzn) > 100.0 * rz0) {
-        flag = kFlagGrowth;
-        break;
-      }
-      const double beta = rzn / rz;
-      rz = rzn;
-      // (every slice's SpMV of this iteration read p before the pAp dot's cluster barrier)
-      for (int t = lo + threadIdx.x; t < hi; t += blockDim.x) p[t] = z[t] + beta * p[t];
-      cl.sync();  // the new p is complete
     }
   }
-  if (flag && rank == 0 && threadIdx.x == 0) atomicOr(a.flags + pair, flag);
-  if (a.update) {
-    const size_t o = static_cast<size_t>(pair) * M;
-    bool bad = false;
-    for (int t = lo + threadIdx.x; t < hi; t += blockDim.x) {
-      bad = bad || !isfinite(x[t]);
-      if ((a.active >> ((t % 6) >> 1)) & 1) a.delta[o + t] += x[t];
-      a.total[o + t] = a.base[o + t] + a.delta[o + t];
-    }
-    if (bad) atomicOr(a.flags + pair, kFlagStep);
+  if (final_step) {
+    __syncthreads();
+    pcg_apply_step(a, P, n, act);
   }
-  cl.sync();  // no CTA leaves while a partner may still read its shared partials
 }
 
 }  // namespace
@@ -723,17 +785,18 @@ void launch_schwarz(const SwzArgs& a_in, int B, cudaStream_t s) {
   }
 }
 
+int pcg_tiles(int gw, int gh) { return (gw + kPcgTile - 1) / kPcgTile * gh; }
+
 void launch_pcg_global(const PcgArgs& a, int B, cudaStream_t s) {
-  static const int sms = [] {
-    int dev = 0, n = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    return n;
-  }();
-  if (B < sms)  // fewer pairs than SMs: a cluster of CTAs per pair
-    k_pcg_cluster<<<B * kPcgCluster, kPcgClusterThreads, 0, s>>>(a);
-  else
-    k_pcg_global<<<B, kPcgThreads, 0, s>>>(a);
+  const dim3 grid(static_cast<unsigned>((pcg_tiles(a.gw, a.gh) + kPcgWarps - 1) / kPcgWarps), static_cast<unsigned>(B));
+  k_pcg_init<<<grid, kPcgThreads, 0, s>>>(a);
+  for (int it = 0; it < a.iters; ++it) {
+    double* prev = it & 1 ? a.p2 : a.p;
+    double* next = it & 1 ? a.p : a.p2;
+    k_pcg_spmv<<<grid, kPcgThreads, 0, s>>>(a, prev, next);
+    k_pcg_update<<<grid, kPcgThreads, 0, s>>>(a, next, it);
+  }
 }
+int pcg_launches(int iters) { return 1 + 2 * iters; }
 
 }  // namespace hwf

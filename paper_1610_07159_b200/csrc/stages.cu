@@ -286,11 +286,17 @@ int hwf_pcg(hwf_ctx* ctx, int gw, int gh, const double* blocks, const double* rh
     std::vector<double> sys;
     pack_system(gw, gh, blocks, rhs, sys);
     const size_t G = static_cast<size_t>(gw) * gh;
+    std::vector<double> soa(sys.size());  // the global PCG reads entry-major records
+    for (size_t n = 0; n < G; ++n)
+      for (int e = 0; e < kSysStride; ++e) soa[e * G + n] = sys[n * kSysStride + e];
     PcgArgs a{};
     a.gw = gw; a.gh = gh; a.iters = iters;
-    a.sys = up(m, sys.data(), sys.size());
+    a.sys = up(m, soa.data(), soa.size());
     a.x = m.alloc<double>(6 * G); a.r = m.alloc<double>(6 * G); a.z = m.alloc<double>(6 * G);
-    a.p = m.alloc<double>(6 * G); a.ap = m.alloc<double>(6 * G);
+    a.p = m.alloc<double>(6 * G); a.ap = m.alloc<double>(6 * G); a.p2 = m.alloc<double>(6 * G);
+    a.part = m.alloc<double>(2 * static_cast<size_t>(pcg_tiles(gw, gh)));
+    a.state = m.alloc<double>(8);
+    a.count = up<unsigned>(m, nullptr, 1);
     a.trace = trace ? m.alloc<double>(iters + 1) : nullptr;
     a.update = 0;
     a.active = 7;
@@ -368,7 +374,7 @@ int hwf_gn_level_trace(hwf_ctx* ctx, const hwf_level* lv, const double* base, do
     make_energies(m, E, d, 2 * gn_iters);
     int* flags = up<int>(m, nullptr, 1);
     Scratch sc;
-    sc.alloc(m, 1, d.N, d.G, false, false, S->subdomain_px <= 0);
+    sc.alloc(m, 1, d.N, d.G, false, false, S->subdomain_px <= 0, pcg_tiles(d.gw, d.gh));
     Launches LC;
     const bool traced = pcg_trace && S->subdomain_px <= 0 && gn_iters > 0;
     const size_t trace_n = static_cast<size_t>(gn_iters) * (S->pcg_iters + 1);
