@@ -314,7 +314,7 @@ inline void record_gn_level(LevelDev& d, int B, const hwf_energy_params& P, cons
       ga.trace = pcg_trace ? pcg_trace + static_cast<size_t>(it) * (S.pcg_iters + 1) : nullptr;
       ga.delta = d.delta; ga.total = d.total; ga.base = d.base; ga.active = S.active_fields; ga.flags = flags;
       launch_pcg_global(ga, B, st);
-      L.count += pcg_launches(S.pcg_iters);
+      L.count += pcg_launches(d.gw, d.gh, S.pcg_iters);
     }
   }
   if (gn > 0 && energy_after) rec_energy_after(d, B, P, S, dF, gn, E, slot_base, flags, st, L, src8);

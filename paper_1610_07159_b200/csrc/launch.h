@@ -124,7 +124,7 @@ void launch_structw(int w, int h, int gw, int gh, int step, const double* half, 
 // solve.cu
 void launch_schwarz(const SwzArgs& a, int B, cudaStream_t s);
 int pcg_tiles(int gw, int gh);  // tiles of one level (PcgArgs::part rows)
-int pcg_launches(int iters);
+int pcg_launches(int gw, int gh, int iters);
 void launch_pcg_global(const PcgArgs& a, int B, cudaStream_t s);
 
 // maps.cu

@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cstdlib>
 
+
 #include "launch.h"
 
 namespace hwf {
@@ -429,34 +430,34 @@ __global__ void __launch_bounds__(128) k_schwarz22(const SwzArgs a, int nsub, in
 }
 
 // ---- global PCG (subdomain_px = 0; pcg_solve, solver.cpp:365-380; pcg_impl, :320-361) ---------------
-// Three kernels, each spread over (tiles, pairs):
+// One kernel per phase, each spread over (tiles, pairs):
 //   k_pcg_init    x = 0, r = b, z = M r, p = 0                              partials r.z, r.r
 //   k_pcg_spmv    p = z + beta p (tile and halo, staged in shared memory), Ap   partial p.Ap
 //   k_pcg_update  x += alpha p, r -= alpha Ap, z = M r                     partials r.z, r.r
-// A tile is a segment of 32 nodes of one grid row, one warp, one node per lane. The system is
+// A tile is a segment of 32 nodes of one grid row: one warp, one node per lane. The system is
 // entry-major ([entry][node], written so by k_node in this mode), so a lane's 21 loads of a block
 // are 256 B coalesced rows across the warp. Every dot is the same fixed tree: per node
 // ((u0v0 + u1v1) + (u2v2 + u3v3)) + (u4v4 + u5v5) rounded op by op, an xor tree over the 32 lanes,
 // then the pair's tiles in index order (strided over 128 threads, xor trees, the 4 warps in order),
-// summed by whichever CTA of the pair finishes last. The order depends only on the level's tiling:
-// results are bitwise independent of the batch size. The per-pair scalars (rz, alpha, beta, a
-// stop bit) live in `state` between kernels; a pair that meets a divergence condition stops
-// iterating (flag set) and still applies its step at the end.
+// summed by whichever CTA of the pair finishes last, which leaves the scalars (rz, alpha, beta,
+// stop) in `state`. The order depends only on the level's tiling: results are bitwise independent
+// of the batch size. A pair that meets a divergence condition stops iterating (flag set) and still
+// applies its step at the end. (A fused all-iterations variant, one CTA or an 8-CTA cluster per
+// pair, was slower at every level size measured.)
 constexpr int kPcgTile = 32, kPcgWarps = 4, kPcgThreads = 32 * kPcgWarps;
 enum : int { kStRz = 0, kStRz0, kStAlpha, kStBeta, kStStop, kStCount = 8 };
+constexpr int kPhCols = kPcgTile + 4;
 
 struct PcgTile {
-  int b, a0, width, tile, ntiles, nctas;
+  int b, a0, width;
   bool live;
 };
-__device__ __forceinline__ PcgTile pcg_tile(int gw, int gh) {
-  const int tpr = (gw + kPcgTile - 1) / kPcgTile;
+__device__ __forceinline__ int pcg_ntiles(int gw, int gh) { return (gw + kPcgTile - 1) / kPcgTile * gh; }
+__device__ __forceinline__ PcgTile pcg_tile_at(int gw, int gh, int tile) {
+  const int tpr = (gw + kPcgTile - 1) / kPcgTile, nt = tpr * gh;
   PcgTile T;
-  T.ntiles = tpr * gh;
-  T.nctas = (T.ntiles + kPcgWarps - 1) / kPcgWarps;
-  T.tile = blockIdx.x * kPcgWarps + (threadIdx.x >> 5);
-  T.live = T.tile < T.ntiles;
-  const int t = T.live ? T.tile : T.ntiles - 1;
+  T.live = tile < nt;
+  const int t = T.live ? tile : nt - 1;
   T.b = t / tpr;
   T.a0 = (t - T.b * tpr) * kPcgTile;
   T.width = T.live ? min(kPcgTile, gw - T.a0) : 0;
@@ -501,22 +502,25 @@ __device__ __forceinline__ bool pcg_last_cta(unsigned* count, int nctas, int* sf
 
 struct PcgPtr {
   const double* sys;  // entry-major: entry e of node n at sys[e * G + n]
-  double *x, *r, *z, *ap, *part, *st;
+  double *x, *r, *z, *ap, *p, *p2, *part, *st;
   unsigned* cnt;
   double* tr;
   size_t G;
+  int ntiles;
 };
-__device__ __forceinline__ PcgPtr pcg_ptr(const PcgArgs& a, int ntiles) {
-  const int pair = blockIdx.y;
+__device__ __forceinline__ PcgPtr pcg_ptr(const PcgArgs& a, int pair) {
   const size_t G = static_cast<size_t>(a.gw) * a.gh, M = 6 * G;
   PcgPtr P;
   P.G = G;
+  P.ntiles = pcg_ntiles(a.gw, a.gh);
   P.sys = a.sys + pair * G * kSysStride;
   P.x = a.x + pair * M;
   P.r = a.r + pair * M;
   P.z = a.z + pair * M;
   P.ap = a.ap + pair * M;
-  P.part = a.part + static_cast<size_t>(pair) * ntiles * 2;
+  P.p = a.p + pair * M;
+  P.p2 = a.p2 + pair * M;
+  P.part = a.part + static_cast<size_t>(pair) * P.ntiles * 2;
   P.st = a.state + static_cast<size_t>(pair) * kStCount;
   P.cnt = a.count + pair;
   P.tr = a.trace ? a.trace + static_cast<size_t>(pair) * (a.iters + 1) : nullptr;
@@ -553,29 +557,16 @@ __device__ __forceinline__ void pcg_precond(const PcgPtr& P, size_t n, const dou
 // Tile partial of one per-node value (xor tree over the warp); every lane returns it.
 __device__ __forceinline__ double tile_partial(bool act, double v) { return warp_sum(act ? v : 0.0); }
 
-__device__ __forceinline__ void pcg_apply_step(const PcgArgs& a, const PcgPtr& P, size_t n, bool act) {
-  bool bad = false;
-  if (act) {
-    const size_t o = static_cast<size_t>(blockIdx.y) * 6 * P.G + 6 * n;
-#pragma unroll
-    for (int k = 0; k < 6; ++k) {
-      const double xv = P.x[6 * n + k];
-      bad = bad || !isfinite(xv);
-      if ((a.active >> (k >> 1)) & 1) a.delta[o + k] += xv;
-      a.total[o + k] = a.base[o + k] + a.delta[o + k];
-    }
-  }
-  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(a.flags + blockIdx.y, kFlagStep);
+__device__ __forceinline__ size_t tile_node(const PcgArgs& a, const PcgTile& T, int j) {
+  return static_cast<size_t>(T.b) * a.gw + T.a0 + min(j, max(T.width - 1, 0));
 }
 
-__global__ void __launch_bounds__(kPcgThreads) k_pcg_init(const PcgArgs a) {
-  __shared__ double red[kPcgWarps];
-  __shared__ int sflag;
-  const PcgTile T = pcg_tile(a.gw, a.gh);
-  const PcgPtr P = pcg_ptr(a, T.ntiles);
+// ---- per-tile phases (one warp each) ----
+__device__ __forceinline__ void tile_init(const PcgArgs& a, const PcgPtr& P, const PcgTile& T, double& prz,
+                                          double& prr) {
   const int j = threadIdx.x & 31;
   const bool act = j < T.width;
-  const size_t n = static_cast<size_t>(T.b) * a.gw + T.a0 + min(j, max(T.width - 1, 0));
+  const size_t n = tile_node(a, T, j);
   double r[6], z[6];
 #pragma unroll
   for (int k = 0; k < 6; ++k) r[k] = act ? __ldg(P.sys + (kSysRhs + k) * P.G + n) : 0.0;
@@ -585,50 +576,20 @@ __global__ void __launch_bounds__(kPcgThreads) k_pcg_init(const PcgArgs a) {
     st6(P.x + 6 * n, zero);
     st6(P.r + 6 * n, r);
     st6(P.z + 6 * n, z);
-    st6(a.p + static_cast<size_t>(blockIdx.y) * 6 * P.G + 6 * n, zero);
+    st6(P.p + 6 * n, zero);
   }
-  const double prz = tile_partial(act, node_dot(r, z));
-  const double prr = tile_partial(act, node_dot(r, r));
-  if (j == 0 && T.live) {
-    P.part[2 * T.tile] = prz;
-    P.part[2 * T.tile + 1] = prr;
-  }
-  if (pcg_last_cta(P.cnt, T.nctas, &sflag)) {
-    const double rz = pair_total(P.part, T.ntiles, 2, red);
-    const double rr = pair_total(P.part + 1, T.ntiles, 2, red);
-    if (threadIdx.x == 0) {
-      if (P.tr) P.tr[0] = sqrt(rr);
-      P.st[kStRz] = rz;
-      P.st[kStRz0] = fabs(rz);
-      P.st[kStBeta] = 0.0;
-      P.st[kStStop] = rz == 0.0 ? 1.0 : 0.0;  // early return (solver.cpp:334-338)
-      if (rz == 0.0 && P.tr)
-        for (int it = 0; it < a.iters; ++it) P.tr[it + 1] = 0.0;
-    }
-  }
-  if (a.iters == 0 && a.update) {
-    __syncthreads();
-    pcg_apply_step(a, P, n, act);
-  }
+  prz = tile_partial(act, node_dot(r, z));
+  prr = tile_partial(act, node_dot(r, r));
 }
 
-// p_next = z + beta p_prev over the tile and its one-node halo (per-warp shared memory, field-major
-// so lane j reads consecutive words), Ap = A p_next with the 9-slot block SpMV.
-constexpr int kPhCols = kPcgTile + 4;
-__global__ void __launch_bounds__(kPcgThreads) k_pcg_spmv(const PcgArgs a, const double* __restrict__ p_prev,
-                                                         double* __restrict__ p_next) {
-  __shared__ double ph_all[kPcgWarps][3][6][kPhCols];
-  __shared__ double red[kPcgWarps];
-  __shared__ int sflag;
-  const PcgTile T = pcg_tile(a.gw, a.gh);
-  const PcgPtr P = pcg_ptr(a, T.ntiles);
-  if (__ldcg(P.st + kStStop) != 0.0) return;
-  const double beta = __ldcg(P.st + kStBeta);
-  const size_t op = static_cast<size_t>(blockIdx.y) * 6 * P.G;
+// p_next = z + beta p_prev over the tile and its one-node halo (this warp's shared memory,
+// field-major so lane j reads consecutive words), then Ap = A p_next with the 9-slot block SpMV.
+__device__ __forceinline__ double tile_spmv(const PcgArgs& a, const PcgPtr& P, const PcgTile& T, double beta,
+                                            const double* __restrict__ p_prev, double* __restrict__ p_next,
+                                            double (*ph)[6][kPhCols]) {
   const int j = threadIdx.x & 31;
-  double (*ph)[6][kPhCols] = ph_all[threadIdx.x >> 5];
-  // rows b-1..b+1, nodes a0-1 .. a0+width: 6 (width + 2) contiguous doubles per row
-  const int span = 6 * (T.width + 2);
+  const int span = 6 * (T.width + 2);  // rows b-1..b+1, nodes a0-1 .. a0+width
+  __syncwarp();
   for (int row = 0; row < 3; ++row) {
     const int qb = T.b - 1 + row;
     for (int i = j; i < span; i += 32) {
@@ -636,8 +597,8 @@ __global__ void __launch_bounds__(kPcgThreads) k_pcg_spmv(const PcgArgs a, const
       double v = 0.0;
       if (qa >= 0 && qa < a.gw && qb >= 0 && qb < a.gh) {
         const size_t o = 6 * (static_cast<size_t>(qb) * a.gw + qa) + c;
-        v = __ldcg(P.z + o) + beta * __ldcg(p_prev + op + o);  // p = z + beta p (solver.cpp:358)
-        if (row == 1 && col >= 1 && col <= T.width) p_next[op + o] = v;
+        v = __ldcg(P.z + o) + beta * __ldcg(p_prev + o);  // p = z + beta p (solver.cpp:358)
+        if (row == 1 && col >= 1 && col <= T.width) p_next[o] = v;
       }
       ph[row][c][col] = v;
     }
@@ -671,41 +632,19 @@ __global__ void __launch_bounds__(kPcgThreads) k_pcg_spmv(const PcgArgs a, const
 #pragma unroll
   for (int c = 0; c < 6; ++c) pown[c] = ph[1][c][j + 1];
   if (act) st6(P.ap + 6 * n, acc);
-  const double part = tile_partial(act, node_dot(pown, acc));
-  if (j == 0 && T.live) P.part[2 * T.tile] = part;
-  if (pcg_last_cta(P.cnt, T.nctas, &sflag)) {
-    const double pAp = pair_total(P.part, T.ntiles, 2, red);
-    if (threadIdx.x == 0) {
-      if (pAp <= 0.0) {  // solver.cpp:344-346
-        P.st[kStStop] = 1.0;
-        atomicOr(a.flags + blockIdx.y, kFlagCurvature);
-      } else {
-        P.st[kStAlpha] = P.st[kStRz] / pAp;
-      }
-    }
-  }
+  return tile_partial(act, node_dot(pown, acc));
 }
 
-__global__ void __launch_bounds__(kPcgThreads) k_pcg_update(const PcgArgs a, const double* __restrict__ p_cur,
-                                                           int it) {
-  __shared__ double red[kPcgWarps];
-  __shared__ int sflag;
-  const PcgTile T = pcg_tile(a.gw, a.gh);
-  const PcgPtr P = pcg_ptr(a, T.ntiles);
+__device__ __forceinline__ void tile_update(const PcgArgs& a, const PcgPtr& P, const PcgTile& T, double alpha,
+                                            const double* __restrict__ p_cur, bool want_rr, double& prz, double& prr) {
   const int j = threadIdx.x & 31;
   const bool act = j < T.width;
-  const size_t n = static_cast<size_t>(T.b) * a.gw + T.a0 + min(j, max(T.width - 1, 0));
-  const bool final_step = a.update && it == a.iters - 1;
-  if (__ldcg(P.st + kStStop) != 0.0) {
-    if (final_step) pcg_apply_step(a, P, n, act);
-    return;
-  }
-  const double alpha = __ldcg(P.st + kStAlpha);
+  const size_t n = tile_node(a, T, j);
   double r[6] = {0, 0, 0, 0, 0, 0}, z[6];
   if (act) {
     double x[6], p[6], ap[6];
     ld6(P.x + 6 * n, x);
-    ld6(p_cur + static_cast<size_t>(blockIdx.y) * 6 * P.G + 6 * n, p);
+    ld6(p_cur + 6 * n, p);
     ld6(P.r + 6 * n, r);
     ld6(P.ap + 6 * n, ap);
 #pragma unroll
@@ -718,30 +657,114 @@ __global__ void __launch_bounds__(kPcgThreads) k_pcg_update(const PcgArgs a, con
   }
   pcg_precond(P, n, r, z);
   if (act) st6(P.z + 6 * n, z);
-  const double prz = tile_partial(act, node_dot(r, z));
-  const double prr = P.tr ? tile_partial(act, node_dot(r, r)) : 0.0;
-  if (j == 0 && T.live) {
-    P.part[2 * T.tile] = prz;
-    P.part[2 * T.tile + 1] = prr;
+  prz = tile_partial(act, node_dot(r, z));
+  prr = want_rr ? tile_partial(act, node_dot(r, r)) : 0.0;
+}
+
+// delta += x, total = base + delta (solver.cpp:518-523); returns whether any x is non-finite.
+__device__ __forceinline__ bool tile_apply(const PcgArgs& a, const PcgPtr& P, const PcgTile& T, int pair) {
+  const int j = threadIdx.x & 31;
+  bool bad = false;
+  if (j < T.width) {
+    const size_t n = tile_node(a, T, j);
+    const size_t o = static_cast<size_t>(pair) * 6 * P.G + 6 * n;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      const double xv = __ldcg(P.x + 6 * n + k);
+      bad = bad || !isfinite(xv);
+      if ((a.active >> (k >> 1)) & 1) a.delta[o + k] += xv;
+      a.total[o + k] = a.base[o + k] + a.delta[o + k];
+    }
   }
-  if (pcg_last_cta(P.cnt, T.nctas, &sflag)) {
-    const double rzn = pair_total(P.part, T.ntiles, 2, red);
-    const double rr = P.tr ? pair_total(P.part + 1, T.ntiles, 2, red) : 0.0;
+  return __any_sync(0xffffffffu, bad);
+}
+
+__global__ void __launch_bounds__(kPcgThreads) k_pcg_init(const PcgArgs a) {
+  __shared__ double red[kPcgWarps];
+  __shared__ int sflag;
+  const int pair = blockIdx.y, tile = blockIdx.x * kPcgWarps + (threadIdx.x >> 5);
+  const PcgPtr P = pcg_ptr(a, pair);
+  const PcgTile T = pcg_tile_at(a.gw, a.gh, tile);
+  double prz, prr;
+  tile_init(a, P, T, prz, prr);
+  if ((threadIdx.x & 31) == 0 && T.live) {
+    P.part[2 * tile] = prz;
+    P.part[2 * tile + 1] = prr;
+  }
+  if (pcg_last_cta(P.cnt, gridDim.x, &sflag)) {
+    const double rz = pair_total(P.part, P.ntiles, 2, red);
+    const double rr = pair_total(P.part + 1, P.ntiles, 2, red);
     if (threadIdx.x == 0) {
-      if (P.tr) P.tr[it + 1] = sqrt(rr);
-      if (fabs(rzn) > 100.0 * P.st[kStRz0]) {  // solver.cpp:352-355
+      if (P.tr) P.tr[0] = sqrt(rr);
+      P.st[kStRz] = rz;
+      P.st[kStRz0] = fabs(rz);
+      P.st[kStBeta] = 0.0;
+      P.st[kStStop] = rz == 0.0 ? 1.0 : 0.0;  // early return (solver.cpp:334-338)
+      if (rz == 0.0 && P.tr)
+        for (int it = 0; it < a.iters; ++it) P.tr[it + 1] = 0.0;
+    }
+  }
+  if (a.iters == 0 && a.update) {
+    __syncthreads();
+    if (tile_apply(a, P, T, pair) && (threadIdx.x & 31) == 0) atomicOr(a.flags + pair, kFlagStep);
+  }
+}
+
+__global__ void __launch_bounds__(kPcgThreads) k_pcg_spmv(const PcgArgs a, int it) {
+  __shared__ double ph_all[kPcgWarps][3][6][kPhCols];
+  __shared__ double red[kPcgWarps];
+  __shared__ int sflag;
+  const int pair = blockIdx.y, tile = blockIdx.x * kPcgWarps + (threadIdx.x >> 5);
+  const PcgPtr P = pcg_ptr(a, pair);
+  if (__ldcg(P.st + kStStop) != 0.0) return;
+  const PcgTile T = pcg_tile_at(a.gw, a.gh, tile);
+  const double* prev = it & 1 ? P.p2 : P.p;
+  double* next = it & 1 ? P.p : P.p2;
+  const double part = tile_spmv(a, P, T, __ldcg(P.st + kStBeta), prev, next, ph_all[threadIdx.x >> 5]);
+  if ((threadIdx.x & 31) == 0 && T.live) P.part[2 * tile] = part;
+  if (pcg_last_cta(P.cnt, gridDim.x, &sflag)) {
+    const double pAp = pair_total(P.part, P.ntiles, 2, red);
+    if (threadIdx.x == 0) {
+      if (pAp <= 0.0) {  // solver.cpp:344-346
         P.st[kStStop] = 1.0;
-        atomicOr(a.flags + blockIdx.y, kFlagGrowth);
+        atomicOr(a.flags + pair, kFlagCurvature);
       } else {
-        P.st[kStBeta] = rzn / P.st[kStRz];
-        P.st[kStRz] = rzn;
+        P.st[kStAlpha] = P.st[kStRz] / pAp;
       }
     }
   }
-  if (final_step) {
-    __syncthreads();
-    pcg_apply_step(a, P, n, act);
+}
+
+__global__ void __launch_bounds__(kPcgThreads) k_pcg_update(const PcgArgs a, int it) {
+  __shared__ double red[kPcgWarps];
+  __shared__ int sflag;
+  const int pair = blockIdx.y, tile = blockIdx.x * kPcgWarps + (threadIdx.x >> 5);
+  const PcgPtr P = pcg_ptr(a, pair);
+  const PcgTile T = pcg_tile_at(a.gw, a.gh, tile);
+  const bool final_step = a.update && it == a.iters - 1;
+  if (__ldcg(P.st + kStStop) == 0.0) {
+    double prz, prr;
+    tile_update(a, P, T, __ldcg(P.st + kStAlpha), it & 1 ? P.p : P.p2, P.tr != nullptr, prz, prr);
+    if ((threadIdx.x & 31) == 0 && T.live) {
+      P.part[2 * tile] = prz;
+      P.part[2 * tile + 1] = prr;
+    }
+    if (pcg_last_cta(P.cnt, gridDim.x, &sflag)) {
+      const double rzn = pair_total(P.part, P.ntiles, 2, red);
+      const double rr = P.tr ? pair_total(P.part + 1, P.ntiles, 2, red) : 0.0;
+      if (threadIdx.x == 0) {
+        if (P.tr) P.tr[it + 1] = sqrt(rr);
+        if (fabs(rzn) > 100.0 * P.st[kStRz0]) {  // solver.cpp:352-355
+          P.st[kStStop] = 1.0;
+          atomicOr(a.flags + pair, kFlagGrowth);
+        } else {
+          P.st[kStBeta] = rzn / P.st[kStRz];
+          P.st[kStRz] = rzn;
+        }
+      }
+    }
   }
+  if (final_step && tile_apply(a, P, T, pair) && (threadIdx.x & 31) == 0) atomicOr(a.flags + pair, kFlagStep);
 }
 
 }  // namespace
@@ -788,15 +811,16 @@ void launch_schwarz(const SwzArgs& a_in, int B, cudaStream_t s) {
 int pcg_tiles(int gw, int gh) { return (gw + kPcgTile - 1) / kPcgTile * gh; }
 
 void launch_pcg_global(const PcgArgs& a, int B, cudaStream_t s) {
-  const dim3 grid(static_cast<unsigned>((pcg_tiles(a.gw, a.gh) + kPcgWarps - 1) / kPcgWarps), static_cast<unsigned>(B));
+  const int nt = pcg_tiles(a.gw, a.gh);
+  const dim3 grid(static_cast<unsigned>((nt + kPcgWarps - 1) / kPcgWarps), static_cast<unsigned>(B));
   k_pcg_init<<<grid, kPcgThreads, 0, s>>>(a);
   for (int it = 0; it < a.iters; ++it) {
-    double* prev = it & 1 ? a.p2 : a.p;
-    double* next = it & 1 ? a.p : a.p2;
-    k_pcg_spmv<<<grid, kPcgThreads, 0, s>>>(a, prev, next);
-    k_pcg_update<<<grid, kPcgThreads, 0, s>>>(a, next, it);
+    k_pcg_spmv<<<grid, kPcgThreads, 0, s>>>(a, it);
+    k_pcg_update<<<grid, kPcgThreads, 0, s>>>(a, it);
   }
 }
-int pcg_launches(int iters) { return 1 + 2 * iters; }
+int pcg_launches(int gw, int gh, int iters) {
+  return 1 + 2 * iters;
+}
 
 }  // namespace hwf

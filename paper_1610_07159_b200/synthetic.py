@@ -110,12 +110,31 @@ def render_pair(w: int, h: int, s=(0.0, 0.0), m=(0.0, 0.0), d=(0.0, 0.0), seed: 
     return out
 
 
-def webcam_pair(index: int, w: int = 640, h: int = 480) -> tuple[np.ndarray, dict]:
-    """cfg2/cfg4 pair `index`: seed 1610+index, constant s in [0, 8] px (disparity 2s), m in [-4, 4] px."""
+def webcam_truth(index: int) -> dict:
+    """The known constant flow of cfg2/cfg4 pair `index` (halfway convention): s in [0, 4] px
+    (disparity 2s in [0, 8]), m in [-2, 2]^2 px (inter-frame motion 2m in [-4, 4]^2), d = 0."""
     rng = np.random.default_rng(1610 + index)
     s = (float(rng.uniform(0.0, 4.0)), 0.0)
     m = (float(rng.uniform(-2.0, 2.0)), float(rng.uniform(-2.0, 2.0)))
-    return render_pair(w, h, s=s, m=m, seed=1610 + index), {"s": s, "m": m, "d": (0.0, 0.0)}
+    return {"s": s, "m": m, "d": (0.0, 0.0)}
+
+
+def webcam_pair(index: int, w: int = 640, h: int = 480) -> tuple[np.ndarray, dict]:
+    """cfg2/cfg4 pair `index`, seed 1610+index, flow webcam_truth(index)."""
+    gt = webcam_truth(index)
+    return render_pair(w, h, s=gt["s"], m=gt["m"], seed=1610 + index), gt
+
+
+def flow_error(grid_total: np.ndarray, truths: list[dict]) -> dict:
+    """Node error of solved finest warp grids (n, G, 6) against constant known flows: median and
+    90th percentile over all nodes of |s - s_gt| and |m - m_gt| (px)."""
+    g = np.asarray(grid_total).reshape(len(truths), -1, 6)
+    st = np.array([t["s"] for t in truths])[:, None, :]
+    mt = np.array([t["m"] for t in truths])[:, None, :]
+    es = np.hypot(g[..., 0] - st[..., 0], g[..., 1] - st[..., 1])
+    em = np.hypot(g[..., 2] - mt[..., 0], g[..., 3] - mt[..., 1])
+    return {"s_median_px": float(np.median(es)), "s_p90_px": float(np.percentile(es, 90)),
+            "m_median_px": float(np.median(em)), "m_p90_px": float(np.percentile(em, 90))}
 
 
 def constant_pair(w: int = 320, h: int = 240, seed: int = 1610) -> tuple[np.ndarray, dict]:

@@ -258,9 +258,12 @@ def test_cfg2_scale_stereo_modes(device, oracle, mode):
         _check_solve(device, oracle, imgs, EnergyParams.preset("stereo-hq"), S, F)
 
 
-def test_batch_is_bitwise_independent(device):
+@pytest.mark.parametrize("sub", [16, 0])
+def test_batch_is_bitwise_independent(device, sub):
+    """Schwarz sweeps and the global PCG (fixed tile-order dots) give every pair the same bits alone
+    or inside a batch."""
     frames = np.stack([synthetic.webcam_pair(i, 128, 96)[0] for i in range(3)])
-    S = SolveSchedule(levels=3, grid_step=8, pcg_iters=5, patch_iters=5)
+    S = SolveSchedule(levels=3, grid_step=8, pcg_iters=5, patch_iters=5, subdomain_px=sub)
     batch, _ = device.solve_batch(frames, EnergyParams(), S)
     for i in range(3):
         (single,), _ = device.solve_batch(frames[i:i + 1], EnergyParams(), S)
