@@ -14,7 +14,13 @@
 // shows up as a NaN or a mismatch against the unsplit solve.
 // Strip formula (same as csrc/split.cu): tile rows t0 = rank*nty/world,
 // t1 = (rank+1)*nty/world; owned node rows [ceil(t0*tile/step), ceil(t1*tile/step)),
-// with the last rank ending at gh.
+// with the last rank ending at gh. Global-PCG mode (subdomain_px = 0): node rows
+// [rank*gh/world, (rank+1)*gh/world).
+// Global-PCG mode runs pcg_impl (core.cpp, solver.cpp:320-361) phase by phase on the owned
+// rows. Its "pcg_part" partials are the per-unknown products of each dot, rows of 6 gw: after
+// the all-gather every rank sums all 6G of them in index order, the same sequence of
+// additions as the unsplit dot, so the split is bitwise equal to the unsplit solve. z outside
+// the owned and halo rows, and the partials outside the owned rows, are poisoned with NaN.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -40,6 +46,10 @@ struct Lev {
   std::vector<orc::Subdomain> subs;
   std::vector<int> owner, loc;
   std::vector<char> take;
+  // global-PCG split state
+  std::vector<double> px, pr, pz, pp, pap, part;
+  double rz = 0.0, rz0 = 0.0, alpha = 0.0, beta = 0.0;
+  bool stop = false;
 };
 
 int ceil_div(int a, int b) { return (a + b - 1) / b; }
@@ -138,7 +148,6 @@ int hwf_split_create(hwf_ctx* ctx, int w, int h, int dtype, const hwf_energy_par
     if (hwf_validate_params(params) != HWF_OK) throw std::invalid_argument("energy weights must be >= 0");
     if (params->w_epi > 0.0 && !F) throw std::invalid_argument("epipolar term enabled without a fundamental matrix");
     if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("bad rank/world");
-    if (sched->subdomain_px <= 0) throw std::invalid_argument("the strip split needs Schwarz mode (subdomain_px > 0)");
     if (w < 2 || h < 2) throw std::invalid_argument("bad frame dims");
     sp->w = w;
     sp->h = h;
@@ -166,6 +175,11 @@ int hwf_split_create(hwf_ctx* ctx, int w, int h, int dtype, const hwf_energy_par
       sp->gn[l] = orc::gn_for_level(sched, l);
       sp->slot_base[l] = nslots;
       nslots += 2 * sp->gn[l];
+      if (tile <= 0) {  // global-PCG mode: a band of node rows
+        v.n0 = static_cast<int>(static_cast<long long>(rank) * v.gh / world);
+        v.n1 = rank == world - 1 ? v.gh : static_cast<int>(static_cast<long long>(rank + 1) * v.gh / world);
+        continue;
+      }
       const int nty = ((v.gh - 1) * step) / tile + 1;
       const int t0 = static_cast<int>(static_cast<long long>(rank) * nty / world);
       const int t1 = static_cast<int>(static_cast<long long>(rank + 1) * nty / world);
@@ -215,7 +229,16 @@ int hwf_split_buffer(hwf_split* sp, int level, const char* name, void** ptr, lon
     else if (!std::strcmp(name, "delta")) { v.delta.resize(g6); *ptr = v.delta.data(); *count = g6; }
     else if (!std::strcmp(name, "energy")) { *ptr = sp->energy.data(); *count = static_cast<long long>(sp->energy.size()); }
     else if (!std::strcmp(name, "flags")) { *ptr = &sp->flags; *count = 1; }
+    else if (!std::strcmp(name, "z")) { v.pz.resize(g6); *ptr = v.pz.data(); *count = g6; }
+    else if (!std::strcmp(name, "pcg_part")) { v.part.resize(g6); *ptr = v.part.data(); *count = g6; }
     else throw std::invalid_argument(std::string("unknown split buffer ") + name);
+  });
+}
+
+int hwf_split_row_elems(hwf_split* sp, int level, const char* name, long long* elems) {
+  return guard(sp, [&] {
+    if (level < 0 || level >= sp->L || !name || !elems) throw std::invalid_argument("bad row query");
+    *elems = 6LL * sp->lev[level].gw;  // every buffer, "pcg_part" included, has 6 gw per node row
   });
 }
 
@@ -240,6 +263,7 @@ int hwf_split_begin(hwf_split* sp, const hwf_frame4* frame) {
 int hwf_split_level_begin(hwf_split* sp, int l) {  // hierarchy.cpp run_scene_flow, one level's setup
   return guard(sp, [&] {
     if (l < 0 || l >= sp->L) throw std::invalid_argument("level out of range");
+    if (sp->flags) return;  // diverged: finish reports it; NaN flows must not reach the maps
     Lev& v = sp->lev[l];
     const size_t g6 = 6 * static_cast<size_t>(v.G);
     v.base.assign(g6, 0.0);
@@ -273,6 +297,7 @@ int hwf_split_level_begin(hwf_split* sp, int l) {  // hierarchy.cpp run_scene_fl
 int hwf_split_linearize(hwf_split* sp, int l, int it) {  // solver.cpp:497-511
   return guard(sp, [&] {
     if (l < 0 || l >= sp->L || it < 0 || it >= sp->gn[l]) throw std::invalid_argument("bad level/iteration");
+    if (sp->flags) return;
     Lev& v = sp->lev[l];
     for (size_t i = 0; i < v.total.size(); ++i) v.total[i] = v.base[i] + v.delta[i];
     if (it > 0) sp->energy[sp->slot_base[l] + 2 * (it - 1) + 1] = owned_energy(sp, l);  // E_after(it-1)
@@ -291,6 +316,7 @@ int hwf_split_linearize(hwf_split* sp, int l, int it) {  // solver.cpp:497-511
 
 int hwf_split_sweep(hwf_split* sp, int l, int s) {  // solver.cpp:430-480, this rank's subdomains
   return guard(sp, [&] {
+    if (sp->S.subdomain_px <= 0) throw std::invalid_argument("hwf_split_sweep needs Schwarz mode");
     if (l < 0 || l >= sp->L || s < 0 || s >= sp->S.patch_iters) throw std::invalid_argument("bad level/sweep");
     Lev& v = sp->lev[l];
     const size_t g6 = 6 * static_cast<size_t>(v.G);
@@ -319,9 +345,128 @@ int hwf_split_sweep(hwf_split* sp, int l, int s) {  // solver.cpp:430-480, this 
   });
 }
 
+namespace {
+void poison_outside(std::vector<double>& v, size_t lo, size_t hi) {
+  for (size_t i = 0; i < v.size(); ++i)
+    if (i < lo || i >= hi) v[i] = std::numeric_limits<double>::quiet_NaN();
+}
+void apply_step(hwf_split* sp, Lev& v) {  // solver.cpp:515-521 for the owned nodes
+  for (int n = v.n0 * v.gw; n < v.n1 * v.gw; ++n)
+    for (int c = 0; c < 6; ++c) {
+      const size_t o = 6 * static_cast<size_t>(n) + c;
+      if (!std::isfinite(v.px[o])) flag(sp, "non-finite Gauss-Newton update");
+      if ((sp->S.active_fields >> (c >> 1)) & 1) v.delta[o] += v.px[o];
+      v.total[o] = v.base[o] + v.delta[o];
+    }
+}
+void precond_rows(const orc::System& S, const std::vector<double>& r, std::vector<double>& z, int n_lo, int n_hi) {
+  for (int n = n_lo; n < n_hi; ++n)  // System::precondition, owned nodes
+    for (int f = 0; f < 3; ++f) {
+      const double* M = &S.pre[(static_cast<size_t>(n) * 3 + f) * 4];
+      const size_t o = 6 * static_cast<size_t>(n) + 2 * f;
+      z[o] = M[0] * r[o] + M[1] * r[o + 1];
+      z[o + 1] = M[2] * r[o] + M[3] * r[o + 1];
+    }
+}
+}  // namespace
+
+int hwf_split_pcg(hwf_split* sp, int l, int phase, int it) {
+  return guard(sp, [&] {
+    if (sp->S.subdomain_px > 0) throw std::invalid_argument("hwf_split_pcg needs global-PCG mode");
+    if (l < 0 || l >= sp->L || phase < 0 || phase > 2 || (phase > 0 && (it < 0 || it >= sp->S.pcg_iters)))
+      throw std::invalid_argument("bad PCG phase");
+    if (sp->flags) return;
+    Lev& v = sp->lev[l];
+    const size_t g6 = 6 * static_cast<size_t>(v.G);
+    const int n_lo = v.n0 * v.gw, n_hi = v.n1 * v.gw;
+    const size_t lo = 6 * static_cast<size_t>(n_lo), hi = 6 * static_cast<size_t>(n_hi);
+    const bool last = phase == 2 && it == sp->S.pcg_iters - 1;
+    if (v.sys.G() != v.G) return;  // linearisation failed (flagged)
+    if (phase == 0) {  // x = 0, r = b, z = M r, p = 0 (pcg_impl with a zero start)
+      for (auto* b : {&v.px, &v.pr, &v.pz, &v.pp, &v.pap, &v.part}) b->assign(g6, 0.0);
+      for (size_t i = lo; i < hi; ++i) v.pr[i] = v.sys.rhs[i];
+      precond_rows(v.sys, v.pr, v.pz, n_lo, n_hi);
+      for (size_t i = lo; i < hi; ++i) v.part[i] = v.pr[i] * v.pz[i];
+      poison_outside(v.part, lo, hi);
+      v.stop = false;
+      if (sp->S.pcg_iters == 0) apply_step(sp, v);
+      return;
+    }
+    if (v.stop) {
+      if (last) apply_step(sp, v);
+      return;
+    }
+    if (phase == 1) {  // p = z (it = 0) or z + beta p over the owned and halo rows, then A p
+      const size_t hlo = 6 * static_cast<size_t>(std::max(0, v.n0 - 1)) * v.gw;
+      const size_t hhi = 6 * static_cast<size_t>(std::min(v.gh, v.n1 + 1)) * v.gw;
+      std::vector<double> z = v.pz;
+      poison_outside(z, hlo, hhi);
+      for (size_t i = hlo; i < hhi; ++i) v.pp[i] = it == 0 ? z[i] : z[i] + v.beta * v.pp[i];
+      std::vector<double> p = v.pp;
+      poison_outside(p, hlo, hhi);
+      for (int n = n_lo; n < n_hi; ++n) {  // System::apply, owned nodes
+        double acc[6] = {0, 0, 0, 0, 0, 0};
+        for (int dy = -1; dy <= 1; ++dy)
+          for (int dx = -1; dx <= 1; ++dx) {
+            const int nb = v.sys.neighbor(n, dx, dy);
+            if (nb < 0) continue;
+            const double* B = v.sys.block(n, orc::slot(dx, dy));
+            for (int i = 0; i < 6; ++i)
+              for (int j = 0; j < 6; ++j) acc[i] += B[6 * i + j] * p[6 * static_cast<size_t>(nb) + j];
+          }
+        for (int i = 0; i < 6; ++i) v.pap[6 * static_cast<size_t>(n) + i] = acc[i];
+      }
+      for (size_t i = lo; i < hi; ++i) v.part[i] = v.pp[i] * v.pap[i];
+      poison_outside(v.part, lo, hi);
+      return;
+    }
+    for (size_t i = lo; i < hi; ++i) {  // x += alpha p, r -= alpha A p, z = M r
+      v.px[i] += v.alpha * v.pp[i];
+      v.pr[i] -= v.alpha * v.pap[i];
+    }
+    precond_rows(v.sys, v.pr, v.pz, n_lo, n_hi);
+    for (size_t i = lo; i < hi; ++i) v.part[i] = v.pr[i] * v.pz[i];
+    poison_outside(v.part, lo, hi);
+    if (last) apply_step(sp, v);
+  });
+}
+
+int hwf_split_pcg_scalars(hwf_split* sp, int l, int phase, int it) {
+  return guard(sp, [&] {
+    if (sp->S.subdomain_px > 0) throw std::invalid_argument("hwf_split_pcg_scalars needs global-PCG mode");
+    if (l < 0 || l >= sp->L || phase < 0 || phase > 2) throw std::invalid_argument("bad PCG phase");
+    (void)it;
+    Lev& v = sp->lev[l];
+    if (v.sys.G() != v.G || (phase > 0 && v.stop)) return;
+    double s = 0.0;  // the unsplit dot's additions, in index order
+    for (double x : v.part) s += x;
+    if (phase == 0) {
+      v.rz = s;
+      v.rz0 = std::abs(s);
+      v.stop = v.rz0 == 0.0;  // solver.cpp:334-338
+    } else if (phase == 1) {
+      if (s <= 0.0) {
+        flag(sp, "PCG: non-positive curvature, system not SPD");
+        v.stop = true;
+      } else {
+        v.alpha = v.rz / s;
+      }
+    } else {
+      if (std::abs(s) > 100.0 * v.rz0) {
+        flag(sp, "PCG: preconditioned residual grew by more than 10x");
+        v.stop = true;
+      } else {
+        v.beta = s / v.rz;
+        v.rz = s;
+      }
+    }
+  });
+}
+
 int hwf_split_energy_after(hwf_split* sp, int l) {
   return guard(sp, [&] {
     if (l < 0 || l >= sp->L) throw std::invalid_argument("level out of range");
+    if (sp->flags) return;  // diverged: finish reports it; NaN flows must not reach the maps
     Lev& v = sp->lev[l];
     for (size_t i = 0; i < v.total.size(); ++i) v.total[i] = v.base[i] + v.delta[i];
     if (sp->gn[l] > 0) sp->energy[sp->slot_base[l] + 2 * (sp->gn[l] - 1) + 1] = owned_energy(sp, l);
@@ -331,6 +476,7 @@ int hwf_split_energy_after(hwf_split* sp, int l) {
 int hwf_split_level_end(hwf_split* sp, int l) {
   return guard(sp, [&] {
     if (l < 0 || l >= sp->L) throw std::invalid_argument("level out of range");
+    if (sp->flags) return;  // diverged: finish reports it; NaN flows must not reach the maps
     Lev& v = sp->lev[l];
     for (size_t i = 0; i < v.total.size(); ++i) v.total[i] = v.base[i] + v.delta[i];
     v.occ.assign(v.N, 0);
@@ -347,7 +493,7 @@ int hwf_split_finish(hwf_split* sp, hwf_result* out, hwf_stats* stats) {
   return guard(sp, [&] {
     const Lev& v = sp->lev[0];
     const orc::GridDims g0 = orc::grid_dims(v.w, v.h, sp->S.grid_step);
-    if (out)
+    if (out && !sp->flags)  // (a diverged split stops before the maps; only the grid is returned)
       for (int pix = 0; pix < v.N; ++pix) {  // pin C.7
         double fl[6];
         orc::interpolate(g0, v.total.data(), pix % v.w, pix / v.w, fl);

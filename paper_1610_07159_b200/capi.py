@@ -164,6 +164,9 @@ _SPLIT_SIGS = {  # include/hwflow_split.h (both the CUDA library and the oracle)
     "hwf_split_level_begin": (C.c_int, [C.c_void_p, C.c_int]),
     "hwf_split_linearize": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
     "hwf_split_sweep": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
+    "hwf_split_row_elems": (C.c_int, [C.c_void_p, C.c_int, C.c_char_p, C.POINTER(C.c_longlong)]),
+    "hwf_split_pcg": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int]),
+    "hwf_split_pcg_scalars": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int]),
     "hwf_split_energy_after": (C.c_int, [C.c_void_p, C.c_int]),
     "hwf_split_level_end": (C.c_int, [C.c_void_p, C.c_int]),
     "hwf_split_finish": (C.c_int, [C.c_void_p, C.POINTER(ResultC), C.POINTER(StatsC)]),

@@ -102,6 +102,10 @@ struct PcgArgs {
   const double* base;
   uint32_t active;
   int* flags;
+  // strip split (hwflow_split.h): tiles [t0, t1) of own node rows [row_lo, row_hi); totals come
+  // from k_pcg_scalars after the driver all-gathers the partials. t1 <= 0: the whole level.
+  int t0, t1, row_lo, row_hi;
+  int split;
 };
 
 // once per device, outside any stream capture
@@ -126,6 +130,8 @@ void launch_schwarz(const SwzArgs& a, int B, cudaStream_t s);
 int pcg_tiles(int gw, int gh);  // tiles of one level (PcgArgs::part rows)
 int pcg_launches(int gw, int gh, int iters);
 void launch_pcg_global(const PcgArgs& a, int B, cudaStream_t s);
+void launch_pcg_phase(const PcgArgs& a, int phase, int it, cudaStream_t s);  // split, B = 1
+void launch_pcg_scalars(const PcgArgs& a, int phase, int it, cudaStream_t s);
 
 // maps.cu
 void launch_pyr_in(const void* src, int dtype, double* dst, long long n, cudaStream_t s);

@@ -453,10 +453,10 @@ struct PcgTile {
   bool live;
 };
 __device__ __forceinline__ int pcg_ntiles(int gw, int gh) { return (gw + kPcgTile - 1) / kPcgTile * gh; }
-__device__ __forceinline__ PcgTile pcg_tile_at(int gw, int gh, int tile) {
+__device__ __forceinline__ PcgTile pcg_tile_at(int gw, int gh, int tile, int t_end) {
   const int tpr = (gw + kPcgTile - 1) / kPcgTile, nt = tpr * gh;
   PcgTile T;
-  T.live = tile < nt;
+  T.live = tile < min(nt, t_end);
   const int t = T.live ? tile : nt - 1;
   T.b = t / tpr;
   T.a0 = (t - T.b * tpr) * kPcgTile;
@@ -577,6 +577,9 @@ __device__ __forceinline__ void tile_init(const PcgArgs& a, const PcgPtr& P, con
     st6(P.r + 6 * n, r);
     st6(P.z + 6 * n, z);
     st6(P.p + 6 * n, zero);
+    // strip split: the search direction of the halo rows starts at zero here too (tile_spmv keeps it)
+    if (T.b == a.row_lo && a.row_lo > 0) st6(P.p + 6 * (n - a.gw), zero);
+    if (T.b == a.row_hi - 1 && a.row_hi < a.gh) st6(P.p + 6 * (n + a.gw), zero);
   }
   prz = tile_partial(act, node_dot(r, z));
   prr = tile_partial(act, node_dot(r, r));
@@ -598,7 +601,11 @@ __device__ __forceinline__ double tile_spmv(const PcgArgs& a, const PcgPtr& P, c
       if (qa >= 0 && qa < a.gw && qb >= 0 && qb < a.gh) {
         const size_t o = 6 * (static_cast<size_t>(qb) * a.gw + qa) + c;
         v = __ldcg(P.z + o) + beta * __ldcg(p_prev + o);  // p = z + beta p (solver.cpp:358)
-        if (row == 1 && col >= 1 && col <= T.width) p_next[o] = v;
+        // own row; in a strip split also the halo rows, which the neighbouring rank owns: the
+        // same z + beta p from the exchanged z, so only z crosses ranks
+        const bool keep = row == 1 || (row == 0 && T.b == a.row_lo && a.row_lo > 0) ||
+                          (row == 2 && T.b == a.row_hi - 1 && a.row_hi < a.gh);
+        if (keep && col >= 1 && col <= T.width) p_next[o] = v;
       }
       ph[row][c][col] = v;
     }
@@ -679,31 +686,59 @@ __device__ __forceinline__ bool tile_apply(const PcgArgs& a, const PcgPtr& P, co
   return __any_sync(0xffffffffu, bad);
 }
 
+// Pair totals -> scalars (the last CTA of a phase, or k_pcg_scalars after a split's all-gather).
+__device__ __forceinline__ void finish_init(const PcgArgs& a, const PcgPtr& P, double* red) {
+  const double rz = pair_total(P.part, P.ntiles, 2, red);
+  const double rr = pair_total(P.part + 1, P.ntiles, 2, red);
+  if (threadIdx.x == 0) {
+    if (P.tr) P.tr[0] = sqrt(rr);
+    P.st[kStRz] = rz;
+    P.st[kStRz0] = fabs(rz);
+    P.st[kStBeta] = 0.0;
+    P.st[kStStop] = rz == 0.0 ? 1.0 : 0.0;  // early return (solver.cpp:334-338)
+    if (rz == 0.0 && P.tr)
+      for (int it = 0; it < a.iters; ++it) P.tr[it + 1] = 0.0;
+  }
+}
+__device__ __forceinline__ void finish_spmv(const PcgArgs& a, const PcgPtr& P, int pair, double* red) {
+  const double pAp = pair_total(P.part, P.ntiles, 2, red);
+  if (threadIdx.x == 0) {
+    if (pAp <= 0.0) {  // solver.cpp:344-346
+      P.st[kStStop] = 1.0;
+      atomicOr(a.flags + pair, kFlagCurvature);
+    } else {
+      P.st[kStAlpha] = P.st[kStRz] / pAp;
+    }
+  }
+}
+__device__ __forceinline__ void finish_update(const PcgArgs& a, const PcgPtr& P, int pair, int it, double* red) {
+  const double rzn = pair_total(P.part, P.ntiles, 2, red);
+  const double rr = P.tr ? pair_total(P.part + 1, P.ntiles, 2, red) : 0.0;
+  if (threadIdx.x == 0) {
+    if (P.tr) P.tr[it + 1] = sqrt(rr);
+    if (fabs(rzn) > 100.0 * P.st[kStRz0]) {  // solver.cpp:352-355
+      P.st[kStStop] = 1.0;
+      atomicOr(a.flags + pair, kFlagGrowth);
+    } else {
+      P.st[kStBeta] = rzn / P.st[kStRz];
+      P.st[kStRz] = rzn;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kPcgThreads) k_pcg_init(const PcgArgs a) {
   __shared__ double red[kPcgWarps];
   __shared__ int sflag;
-  const int pair = blockIdx.y, tile = blockIdx.x * kPcgWarps + (threadIdx.x >> 5);
+  const int pair = blockIdx.y, tile = a.t0 + blockIdx.x * kPcgWarps + (threadIdx.x >> 5);
   const PcgPtr P = pcg_ptr(a, pair);
-  const PcgTile T = pcg_tile_at(a.gw, a.gh, tile);
+  const PcgTile T = pcg_tile_at(a.gw, a.gh, tile, a.t1);
   double prz, prr;
   tile_init(a, P, T, prz, prr);
   if ((threadIdx.x & 31) == 0 && T.live) {
     P.part[2 * tile] = prz;
     P.part[2 * tile + 1] = prr;
   }
-  if (pcg_last_cta(P.cnt, gridDim.x, &sflag)) {
-    const double rz = pair_total(P.part, P.ntiles, 2, red);
-    const double rr = pair_total(P.part + 1, P.ntiles, 2, red);
-    if (threadIdx.x == 0) {
-      if (P.tr) P.tr[0] = sqrt(rr);
-      P.st[kStRz] = rz;
-      P.st[kStRz0] = fabs(rz);
-      P.st[kStBeta] = 0.0;
-      P.st[kStStop] = rz == 0.0 ? 1.0 : 0.0;  // early return (solver.cpp:334-338)
-      if (rz == 0.0 && P.tr)
-        for (int it = 0; it < a.iters; ++it) P.tr[it + 1] = 0.0;
-    }
-  }
+  if (!a.split && pcg_last_cta(P.cnt, gridDim.x, &sflag)) finish_init(a, P, red);
   if (a.iters == 0 && a.update) {
     __syncthreads();
     if (tile_apply(a, P, T, pair) && (threadIdx.x & 31) == 0) atomicOr(a.flags + pair, kFlagStep);
@@ -714,33 +749,23 @@ __global__ void __launch_bounds__(kPcgThreads) k_pcg_spmv(const PcgArgs a, int i
   __shared__ double ph_all[kPcgWarps][3][6][kPhCols];
   __shared__ double red[kPcgWarps];
   __shared__ int sflag;
-  const int pair = blockIdx.y, tile = blockIdx.x * kPcgWarps + (threadIdx.x >> 5);
+  const int pair = blockIdx.y, tile = a.t0 + blockIdx.x * kPcgWarps + (threadIdx.x >> 5);
   const PcgPtr P = pcg_ptr(a, pair);
   if (__ldcg(P.st + kStStop) != 0.0) return;
-  const PcgTile T = pcg_tile_at(a.gw, a.gh, tile);
+  const PcgTile T = pcg_tile_at(a.gw, a.gh, tile, a.t1);
   const double* prev = it & 1 ? P.p2 : P.p;
   double* next = it & 1 ? P.p : P.p2;
   const double part = tile_spmv(a, P, T, __ldcg(P.st + kStBeta), prev, next, ph_all[threadIdx.x >> 5]);
   if ((threadIdx.x & 31) == 0 && T.live) P.part[2 * tile] = part;
-  if (pcg_last_cta(P.cnt, gridDim.x, &sflag)) {
-    const double pAp = pair_total(P.part, P.ntiles, 2, red);
-    if (threadIdx.x == 0) {
-      if (pAp <= 0.0) {  // solver.cpp:344-346
-        P.st[kStStop] = 1.0;
-        atomicOr(a.flags + pair, kFlagCurvature);
-      } else {
-        P.st[kStAlpha] = P.st[kStRz] / pAp;
-      }
-    }
-  }
+  if (!a.split && pcg_last_cta(P.cnt, gridDim.x, &sflag)) finish_spmv(a, P, pair, red);
 }
 
 __global__ void __launch_bounds__(kPcgThreads) k_pcg_update(const PcgArgs a, int it) {
   __shared__ double red[kPcgWarps];
   __shared__ int sflag;
-  const int pair = blockIdx.y, tile = blockIdx.x * kPcgWarps + (threadIdx.x >> 5);
+  const int pair = blockIdx.y, tile = a.t0 + blockIdx.x * kPcgWarps + (threadIdx.x >> 5);
   const PcgPtr P = pcg_ptr(a, pair);
-  const PcgTile T = pcg_tile_at(a.gw, a.gh, tile);
+  const PcgTile T = pcg_tile_at(a.gw, a.gh, tile, a.t1);
   const bool final_step = a.update && it == a.iters - 1;
   if (__ldcg(P.st + kStStop) == 0.0) {
     double prz, prr;
@@ -749,22 +774,22 @@ __global__ void __launch_bounds__(kPcgThreads) k_pcg_update(const PcgArgs a, int
       P.part[2 * tile] = prz;
       P.part[2 * tile + 1] = prr;
     }
-    if (pcg_last_cta(P.cnt, gridDim.x, &sflag)) {
-      const double rzn = pair_total(P.part, P.ntiles, 2, red);
-      const double rr = P.tr ? pair_total(P.part + 1, P.ntiles, 2, red) : 0.0;
-      if (threadIdx.x == 0) {
-        if (P.tr) P.tr[it + 1] = sqrt(rr);
-        if (fabs(rzn) > 100.0 * P.st[kStRz0]) {  // solver.cpp:352-355
-          P.st[kStStop] = 1.0;
-          atomicOr(a.flags + pair, kFlagGrowth);
-        } else {
-          P.st[kStBeta] = rzn / P.st[kStRz];
-          P.st[kStRz] = rzn;
-        }
-      }
-    }
+    if (!a.split && pcg_last_cta(P.cnt, gridDim.x, &sflag)) finish_update(a, P, pair, it, red);
   }
   if (final_step && tile_apply(a, P, T, pair) && (threadIdx.x & 31) == 0) atomicOr(a.flags + pair, kFlagStep);
+}
+
+// Strip split: the scalars of a phase from the all-gathered partials of every rank (same tree).
+__global__ void __launch_bounds__(kPcgThreads) k_pcg_scalars(const PcgArgs a, int phase, int it) {
+  __shared__ double red[kPcgWarps];
+  const int pair = blockIdx.x;
+  const PcgPtr P = pcg_ptr(a, pair);
+  if (phase == 0) {
+    finish_init(a, P, red);
+  } else if (__ldcg(P.st + kStStop) == 0.0) {
+    if (phase == 1) finish_spmv(a, P, pair, red);
+    else finish_update(a, P, pair, it, red);
+  }
 }
 
 }  // namespace
@@ -810,14 +835,41 @@ void launch_schwarz(const SwzArgs& a_in, int B, cudaStream_t s) {
 
 int pcg_tiles(int gw, int gh) { return (gw + kPcgTile - 1) / kPcgTile * gh; }
 
-void launch_pcg_global(const PcgArgs& a, int B, cudaStream_t s) {
-  const int nt = pcg_tiles(a.gw, a.gh);
-  const dim3 grid(static_cast<unsigned>((nt + kPcgWarps - 1) / kPcgWarps), static_cast<unsigned>(B));
+namespace {
+PcgArgs whole(const PcgArgs& in) {
+  PcgArgs a = in;
+  if (a.t1 <= 0) {
+    a.t0 = 0;
+    a.t1 = pcg_tiles(a.gw, a.gh);
+    a.row_lo = 0;
+    a.row_hi = a.gh;
+  }
+  return a;
+}
+dim3 pcg_grid(const PcgArgs& a, int B) {
+  return dim3(static_cast<unsigned>(std::max(1, (a.t1 - a.t0 + kPcgWarps - 1) / kPcgWarps)), static_cast<unsigned>(B));
+}
+}  // namespace
+
+void launch_pcg_global(const PcgArgs& a_in, int B, cudaStream_t s) {
+  const PcgArgs a = whole(a_in);
+  const dim3 grid = pcg_grid(a, B);
   k_pcg_init<<<grid, kPcgThreads, 0, s>>>(a);
   for (int it = 0; it < a.iters; ++it) {
     k_pcg_spmv<<<grid, kPcgThreads, 0, s>>>(a, it);
     k_pcg_update<<<grid, kPcgThreads, 0, s>>>(a, it);
   }
+}
+void launch_pcg_phase(const PcgArgs& a_in, int phase, int it, cudaStream_t s) {
+  const PcgArgs a = whole(a_in);
+  if (a.t1 <= a.t0) return;  // this rank owns no rows at this level
+  const dim3 grid = pcg_grid(a, 1);
+  if (phase == 0) k_pcg_init<<<grid, kPcgThreads, 0, s>>>(a);
+  else if (phase == 1) k_pcg_spmv<<<grid, kPcgThreads, 0, s>>>(a, it);
+  else k_pcg_update<<<grid, kPcgThreads, 0, s>>>(a, it);
+}
+void launch_pcg_scalars(const PcgArgs& a_in, int phase, int it, cudaStream_t s) {
+  k_pcg_scalars<<<1, kPcgThreads, 0, s>>>(whole(a_in), phase, it);
 }
 int pcg_launches(int gw, int gh, int iters) {
   return 1 + 2 * iters;

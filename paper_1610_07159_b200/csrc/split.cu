@@ -34,17 +34,19 @@ namespace {
 
 int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
-// The strip of `rank` at one level; the same formula runs in oracle/split.cpp.
+// The strip of `rank` at one level; the same formula runs in oracle/split.cpp. Schwarz mode:
+// a band of subdomain tile rows. Global-PCG mode (tile_px = 0): a band of node rows.
 void strip(const LevelDev& d, int tile_px, int rank, int world, Range& R, int& n0, int& n1) {
-  const int nty = d.nty, gh = d.gh, gw = d.gw, step = d.step;
+  const int gh = d.gh, gw = d.gw, step = d.step;
+  const int nty = tile_px > 0 ? d.nty : gh;
   const int t0 = static_cast<int>(static_cast<long long>(rank) * nty / world);
   const int t1 = static_cast<int>(static_cast<long long>(rank + 1) * nty / world);
-  n0 = std::min(gh, ceil_div(t0 * tile_px, step));
-  n1 = rank == world - 1 ? gh : std::min(gh, ceil_div(t1 * tile_px, step));
+  n0 = tile_px > 0 ? std::min(gh, ceil_div(t0 * tile_px, step)) : t0;
+  n1 = rank == world - 1 ? gh : (tile_px > 0 ? std::min(gh, ceil_div(t1 * tile_px, step)) : t1);
   const int rows = ceil_div(d.ncy, d.tcy);
   R.whole = false;
-  R.sub0 = t0 * d.ntx;
-  R.sub1 = t1 * d.ntx;
+  R.sub0 = tile_px > 0 ? t0 * d.ntx : 0;
+  R.sub1 = tile_px > 0 ? t1 * d.ntx : 0;
   R.own_lo = n0 * gw;
   R.own_hi = n1 * gw;
   if (n1 <= n0) {  // nothing owned at this level
@@ -80,7 +82,6 @@ int hwf_split_create(hwf_ctx* ctx, int w, int h, int dtype, const hwf_energy_par
     if (!out) throw InvalidArg("null out");
     check_params(params, sched, F);
     if (world < 1 || rank < 0 || rank >= world) throw InvalidArg("bad rank/world");
-    if (sched->subdomain_px <= 0) throw InvalidArg("the strip split needs Schwarz mode (subdomain_px > 0)");
     if (w < 2 || h < 2) throw InvalidArg("bad frame dims");
     if (dtype != HWF_DTYPE_U8 && dtype != HWF_DTYPE_F64) throw InvalidArg("unknown dtype");
     auto sp = std::make_unique<hwf_split>();
@@ -141,7 +142,19 @@ int hwf_split_buffer(hwf_split* sp, int level, const char* name, void** ptr, lon
     else if (!std::strcmp(name, "delta")) { *ptr = d.delta; *count = g6; }
     else if (!std::strcmp(name, "energy")) { *ptr = p.E.part; *count = p.E.pair_stride(); }
     else if (!std::strcmp(name, "flags")) { *ptr = p.flags; *count = 1; }
+    else if (!std::strcmp(name, "z") && p.sc.pz) { *ptr = p.sc.pz; *count = g6; }
+    else if (!std::strcmp(name, "pcg_part") && p.sc.ppart) { *ptr = p.sc.ppart; *count = 2LL * pcg_tiles(d.gw, d.gh); }
     else throw InvalidArg(std::string("unknown split buffer ") + name);
+  });
+}
+
+int hwf_split_row_elems(hwf_split* sp, int level, const char* name, long long* elems) {
+  return guard(sp ? sp->ctx : nullptr, [&] {
+    checked(sp, level);
+    if (!name || !elems) throw InvalidArg("null row query");
+    const LevelDev& d = sp->plan->lv[level];
+    // the device's PCG partials: 2 per 32-node tile, ceil(gw / 32) tiles per node row
+    *elems = !std::strcmp(name, "pcg_part") ? 2LL * pcg_tiles(d.gw, 1) : 6LL * d.gw;
   });
 }
 
@@ -178,8 +191,46 @@ int hwf_split_linearize(hwf_split* sp, int level, int it) {
 int hwf_split_sweep(hwf_split* sp, int level, int s) {
   return guard(sp ? sp->ctx : nullptr, [&] {
     Plan& p = *checked(sp, level)->plan;
+    if (p.S.subdomain_px <= 0) throw InvalidArg("hwf_split_sweep needs Schwarz mode (subdomain_px > 0)");
     if (s < 0 || s >= p.S.patch_iters) throw InvalidArg("sweep out of range");
     rec_sweep(p.lv[level], 1, p.S, s, p.flags, sp->ctx->stream, sp->LC, &sp->range[level]);
+  });
+}
+
+namespace {
+PcgArgs split_pcg_args(hwf_split* sp, int level) {
+  Plan& p = *sp->plan;
+  LevelDev& d = p.lv[level];
+  PcgArgs ga{};
+  ga.gw = d.gw; ga.gh = d.gh; ga.iters = p.S.pcg_iters; ga.sys = d.sys;
+  ga.x = p.sc.px; ga.r = p.sc.pr; ga.z = p.sc.pz; ga.p = p.sc.pp; ga.ap = p.sc.pap; ga.p2 = p.sc.pp2;
+  ga.part = p.sc.ppart; ga.state = p.sc.pstate; ga.count = p.sc.pcount; ga.update = 1;
+  ga.delta = d.delta; ga.total = d.total; ga.base = d.base; ga.active = p.S.active_fields; ga.flags = p.flags;
+  const int tpr = pcg_tiles(d.gw, 1);
+  ga.t0 = sp->n0[level] * tpr;
+  ga.t1 = sp->n1[level] * tpr;
+  ga.row_lo = sp->n0[level];
+  ga.row_hi = sp->n1[level];
+  ga.split = 1;
+  return ga;
+}
+}  // namespace
+
+int hwf_split_pcg(hwf_split* sp, int level, int phase, int it) {
+  return guard(sp ? sp->ctx : nullptr, [&] {
+    Plan& p = *checked(sp, level)->plan;
+    if (p.S.subdomain_px > 0) throw InvalidArg("hwf_split_pcg needs global-PCG mode (subdomain_px = 0)");
+    if (phase < 0 || phase > 2 || (phase > 0 && (it < 0 || it >= p.S.pcg_iters))) throw InvalidArg("bad PCG phase");
+    launch_pcg_phase(split_pcg_args(sp, level), phase, it, sp->ctx->stream);
+  });
+}
+
+int hwf_split_pcg_scalars(hwf_split* sp, int level, int phase, int it) {
+  return guard(sp ? sp->ctx : nullptr, [&] {
+    Plan& p = *checked(sp, level)->plan;
+    if (p.S.subdomain_px > 0) throw InvalidArg("hwf_split_pcg_scalars needs global-PCG mode");
+    if (phase < 0 || phase > 2) throw InvalidArg("bad PCG phase");
+    launch_pcg_scalars(split_pcg_args(sp, level), phase, it, sp->ctx->stream);
   });
 }
 

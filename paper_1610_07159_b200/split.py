@@ -6,13 +6,17 @@ moves data between ranks.
   - The CPU tests: the oracle (host buffers) on gloo ranks, or on in-process `LocalComm`
     ranks that copy rows directly.
 Collectives and data movement per frame:
-  - After every Schwarz sweep but the last: halo exchange of the published x rows next to
-    each strip (P2P), 2 node rows per rank.
+  - Schwarz mode, after every sweep but the last: halo exchange of the published x rows next
+    to each strip (P2P), 2 node rows per rank.
+  - Global-PCG mode (the headline schedule), per PCG iteration: two all-gathers of the dot
+    partials (each rank's tiles, a few hundred KB at 4K) and one z halo exchange; every rank
+    then sums the same partials in the same order, so the scalars agree bitwise.
   - After every Gauss-Newton iteration: all-gather of the owned total/delta rows. Occlusion,
     illumination, prolongation and the next linearisation read the whole grid.
   - At the end: sum-all-reduce of the energy partials and OR of the divergence flags.
-Schwarz sweeps are Jacobi across subdomains (solver.cpp:430-480), so a split with exact
-halos reproduces the unsplit solve bit for bit.
+Schwarz sweeps are Jacobi across subdomains (solver.cpp:430-480), and the global PCG's dots
+sum per-tile partials in a fixed order, so a split with exact halos reproduces the unsplit solve
+bit for bit in both modes.
 """
 from __future__ import annotations
 
@@ -51,6 +55,9 @@ class SplitRank:
         self._check(self.lib.hwf_split_schedule(self.h, C.byref(L), gn))
         self.levels, self.gn = L.value, [gn[l] for l in range(L.value)]
         self.patch_iters = schedule.patch_iters
+        self.pcg_iters = schedule.pcg_iters
+        self.global_mode = schedule.subdomain_px <= 0
+        self._row_elems = {}
         self.rows = []  # per level: (n0, n1, gw)
         for l in range(self.levels):
             n0, n1, gw = C.c_int(), C.c_int(), C.c_int()
@@ -70,9 +77,17 @@ class SplitRank:
         ct = C.c_int32 if flags else C.c_double
         return torch.from_numpy(np.ctypeslib.as_array(C.cast(p, C.POINTER(ct)), shape=(n.value,)))
 
-    def row_slice(self, level: int, r0: int, r1: int) -> slice:
-        gw = self.rows[level][2]
-        return slice(6 * gw * r0, 6 * gw * r1)
+    def row_elems(self, level: int, name: str = "total") -> int:
+        key = (level, name)
+        if key not in self._row_elems:
+            e = C.c_longlong()
+            self._check(self.lib.hwf_split_row_elems(self.h, level, name.encode(), C.byref(e)))
+            self._row_elems[key] = e.value
+        return self._row_elems[key]
+
+    def row_slice(self, level: int, r0: int, r1: int, name: str = "total") -> slice:
+        w = self.row_elems(level, name)
+        return slice(w * r0, w * r1)
 
     # steps (include/hwflow_split.h)
     def begin(self, frame: Frame4C):
@@ -86,6 +101,12 @@ class SplitRank:
 
     def sweep(self, l: int, s: int):
         self._check(self.lib.hwf_split_sweep(self.h, l, s))
+
+    def pcg(self, l: int, phase: int, it: int = 0):
+        self._check(self.lib.hwf_split_pcg(self.h, l, phase, it))
+
+    def pcg_scalars(self, l: int, phase: int, it: int = 0):
+        self._check(self.lib.hwf_split_pcg_scalars(self.h, l, phase, it))
 
     def energy_after(self, l: int):
         self._check(self.lib.hwf_split_energy_after(self.h, l))
@@ -141,7 +162,7 @@ class LocalComm:
                 for q in (n0 - 1, n1):
                     if 0 <= q < gh:
                         src = ranks[_owner(rows, q)]
-                        sl = r.row_slice(level, q, q + 1)
+                        sl = r.row_slice(level, q, q + 1, name)
                         r.buffer(level, name)[sl].copy_(src.buffer(level, name)[sl])
 
     def allgather_rows(self, ranks: list[SplitRank], level: int, name: str):
@@ -150,7 +171,7 @@ class LocalComm:
                 n0, n1, _ = src.rows[level]
                 if n1 <= n0:
                     continue
-                sl = src.row_slice(level, n0, n1)
+                sl = src.row_slice(level, n0, n1, name)
                 for dst in ranks:
                     if dst is not src:
                         dst.buffer(level, name)[sl].copy_(src.buffer(level, name)[sl])
@@ -209,12 +230,12 @@ class TorchComm:
                 continue
             for tag, q in ((0, n0 - 1), (1, n1)):
                 if 0 <= q < gh and _owner(rows, q) == me.rank:  # r needs my row q
-                    ops.append(dist.P2POp(dist.isend, buf[me.row_slice(level, q, q + 1)], r, self.group, tag))
+                    ops.append(dist.P2POp(dist.isend, buf[me.row_slice(level, q, q + 1, name)], r, self.group, tag))
         n0, n1 = rows[me.rank]
         if n1 > n0:
             for tag, q in ((0, n0 - 1), (1, n1)):
                 if 0 <= q < gh:
-                    ops.append(dist.P2POp(dist.irecv, buf[me.row_slice(level, q, q + 1)], _owner(rows, q),
+                    ops.append(dist.P2POp(dist.irecv, buf[me.row_slice(level, q, q + 1, name)], _owner(rows, q),
                                           self.group, tag))
         if not ops:
             return
@@ -225,20 +246,20 @@ class TorchComm:
     def allgather_rows(self, ranks: list[SplitRank], level: int, name: str):
         (me,) = ranks
         rows = [self.table[r][level] for r in range(self.world)]
-        gw = me.rows[level][2]
-        span = 6 * gw * max(n1 - n0 for n0, n1 in rows)
+        w = me.row_elems(level, name)
+        span = w * max(n1 - n0 for n0, n1 in rows)
         if span == 0:
             return
         buf = me.buffer(level, name)
         with self._streamed(ranks):
             n0, n1 = rows[me.rank]
             slab = torch.zeros(span, dtype=buf.dtype, device=buf.device)
-            slab[: 6 * gw * (n1 - n0)].copy_(buf[me.row_slice(level, n0, n1)])
+            slab[: w * (n1 - n0)].copy_(buf[me.row_slice(level, n0, n1, name)])
             out = torch.empty(self.world * span, dtype=buf.dtype, device=buf.device)
             dist.all_gather_into_tensor(out, slab, group=self.group)
             for r, (a, b) in enumerate(rows):
                 if r != me.rank and b > a:
-                    buf[me.row_slice(level, a, b)].copy_(out[r * span: r * span + 6 * gw * (b - a)])
+                    buf[me.row_slice(level, a, b, name)].copy_(out[r * span: r * span + w * (b - a)])
 
     def allreduce_sum(self, ranks: list[SplitRank], name: str):
         (me,) = ranks
@@ -269,6 +290,24 @@ def _frame(images: np.ndarray) -> tuple[Frame4C, np.ndarray]:
     return f, a
 
 
+def _pcg_split(ranks: list[SplitRank], comm, l: int):
+    """pcg_solve (solver.cpp:365-380) across the strips, include/hwflow_split.h's protocol."""
+    def phase(ph: int, it: int = 0):
+        for r in ranks:
+            r.pcg(l, ph, it)
+        comm.allgather_rows(ranks, l, "pcg_part")
+        for r in ranks:
+            r.pcg_scalars(l, ph, it)
+
+    phase(0)
+    comm.halo(ranks, l, "z")
+    for it in range(ranks[0].pcg_iters):
+        phase(1, it)
+        phase(2, it)
+        if it < ranks[0].pcg_iters - 1:
+            comm.halo(ranks, l, "z")
+
+
 def solve_split(ranks: list[SplitRank], comm, images: np.ndarray) -> list[tuple[FlowResult, GnStats]]:
     """run_scene_flow of one frame pair (4, h, w), split across `ranks`
     (all of them for LocalComm, this process's one for TorchComm). Returns each local rank's
@@ -283,11 +322,14 @@ def solve_split(ranks: list[SplitRank], comm, images: np.ndarray) -> list[tuple[
         for it in range(r0.gn[l]):
             for r in ranks:
                 r.linearize(l, it)
-            for s in range(r0.patch_iters):
-                for r in ranks:
-                    r.sweep(l, s)
-                if s < r0.patch_iters - 1:
-                    comm.halo(ranks, l, r0.lib.hwf_split_swept(s).decode())
+            if r0.global_mode:
+                _pcg_split(ranks, comm, l)
+            else:
+                for s in range(r0.patch_iters):
+                    for r in ranks:
+                        r.sweep(l, s)
+                    if s < r0.patch_iters - 1:
+                        comm.halo(ranks, l, r0.lib.hwf_split_swept(s).decode())
             comm.allgather_rows(ranks, l, "total")
             comm.allgather_rows(ranks, l, "delta")
         for r in ranks:

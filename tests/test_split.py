@@ -24,6 +24,8 @@ from paper_1610_07159_b200.hwflow import EnergyParams, SolveSchedule
 from paper_1610_07159_b200.split import LocalComm, SplitRank, solve_split
 
 SCHED = SolveSchedule(levels=3, grid_step=4, gn_per_level=[2, 2, 2], pcg_iters=4, patch_iters=3, subdomain_px=16)
+GSCHED = SolveSchedule(levels=3, grid_step=4, gn_per_level=[2, 2, 2], pcg_iters=4, subdomain_px=0)  # global PCG
+MODES = {"schwarz": SCHED, "global": GSCHED}
 
 
 def _frames(w=128, h=96, seed=0):
@@ -44,11 +46,12 @@ def _assert_same(split, ref, energy_rtol):
         assert np.allclose(a, b, rtol=energy_rtol, atol=0.0)
 
 
+@pytest.mark.parametrize("mode", ["schwarz", "global"])
 @pytest.mark.parametrize("world", [1, 2, 3, 5])
-def test_split_local_matches_unsplit_oracle(oracle, world):
+def test_split_local_matches_unsplit_oracle(oracle, world, mode):
     imgs = _frames()
-    ref = _unsplit(oracle, imgs, SCHED)
-    ranks = [SplitRank(oracle, 128, 96, DTYPE_U8, EnergyParams(), SCHED, None, r, world) for r in range(world)]
+    ref = _unsplit(oracle, imgs, MODES[mode])
+    ranks = [SplitRank(oracle, 128, 96, DTYPE_U8, EnergyParams(), MODES[mode], None, r, world) for r in range(world)]
     owned = [r.rows[0][:2] for r in ranks]
     assert owned[0][0] == 0 and owned[-1][1] == 25 and all(a[1] == b[0] for a, b in zip(owned, owned[1:]))
     outs = solve_split(ranks, LocalComm(), imgs)
@@ -56,25 +59,34 @@ def test_split_local_matches_unsplit_oracle(oracle, world):
         _assert_same(out, ref, 1e-12 if world > 1 else 0.0)
 
 
-def test_split_detects_a_missing_halo_exchange(oracle):
-    class NoHalo(LocalComm):
-        def halo(self, ranks, level, name):
-            pass
+class _NoHalo(LocalComm):
+    def halo(self, ranks, level, name):
+        pass
 
+
+class _NoPartials(LocalComm):
+    def allgather_rows(self, ranks, level, name):
+        if name != "pcg_part":
+            super().allgather_rows(ranks, level, name)
+
+
+@pytest.mark.parametrize("mode,comm", [("schwarz", _NoHalo), ("global", _NoHalo), ("global", _NoPartials)])
+def test_split_detects_a_missing_exchange(oracle, mode, comm):
     imgs = _frames()
-    ref = _unsplit(oracle, imgs, SCHED)
-    ranks = [SplitRank(oracle, 128, 96, DTYPE_U8, EnergyParams(), SCHED, None, r, 2) for r in range(2)]
+    ref = _unsplit(oracle, imgs, MODES[mode])
+    ranks = [SplitRank(oracle, 128, 96, DTYPE_U8, EnergyParams(), MODES[mode], None, r, 2) for r in range(2)]
     try:
-        (r, _), _ = solve_split(ranks, NoHalo(), imgs)
+        (r, _), _ = solve_split(ranks, comm(), imgs)
         assert not np.array_equal(r.grid_total, ref[0].grid_total)
     except Exception as e:  # NaN from a poisoned row reaching a divergence check
-        assert "diverg" in str(e).lower() or "non-finite" in str(e).lower()
+        assert "diverg" in str(e).lower() or "non-finite" in str(e).lower() or "pcg" in str(e).lower()
 
 
-def test_split_rejects_global_pcg_mode(oracle):
+def test_split_global_mode_rejects_sweeps(oracle):
     from paper_1610_07159_b200.capi import InvalidArgument
+    r = SplitRank(oracle, 128, 96, DTYPE_U8, EnergyParams(), GSCHED, None, 0, 2)
     with pytest.raises(InvalidArgument, match="Schwarz"):
-        SplitRank(oracle, 128, 96, DTYPE_U8, EnergyParams(), SolveSchedule(levels=2, subdomain_px=0), None, 0, 2)
+        r.sweep(0, 0)
 
 
 def _free_port() -> int:
@@ -83,7 +95,7 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _worker(rank: int, ws: int, port: int, q):
+def _worker(rank: int, ws: int, port: int, q, mode: str = "schwarz"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
     dist.init_process_group("gloo", rank=rank, world_size=ws)
@@ -92,7 +104,7 @@ def _worker(rank: int, ws: int, port: int, q):
         from paper_1610_07159_b200.hwflow import Solver
         from paper_1610_07159_b200.split import TorchComm
         solver = Solver(build.ORACLE_LIB)
-        me = SplitRank(solver, 128, 96, DTYPE_U8, EnergyParams(), SCHED, None, rank, ws)
+        me = SplitRank(solver, 128, 96, DTYPE_U8, EnergyParams(), MODES[mode], None, rank, ws)
         ((r, st),) = solve_split([me], TorchComm(me), _frames())
         q.put((rank, r.grid_total, r.vis4, st.energy_before, st.energy_after))
     finally:
@@ -100,13 +112,13 @@ def _worker(rank: int, ws: int, port: int, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("ws", [2, 3])
-def test_split_gloo_ranks_match_unsplit_oracle(oracle, ws):
-    ref = _unsplit(oracle, _frames(), SCHED)
+@pytest.mark.parametrize("ws,mode", [(2, "schwarz"), (3, "schwarz"), (2, "global"), (3, "global")])
+def test_split_gloo_ranks_match_unsplit_oracle(oracle, ws, mode):
+    ref = _unsplit(oracle, _frames(), MODES[mode])
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, ws, port, q)) for r in range(ws)]
+    procs = [ctx.Process(target=_worker, args=(r, ws, port, q, mode)) for r in range(ws)]
     for p in procs:
         p.start()
     got = [q.get(timeout=300) for _ in range(ws)]
@@ -127,6 +139,10 @@ def test_split_gloo_ranks_match_unsplit_oracle(oracle, ws):
     (640, 480, 3, SolveSchedule(levels=4, grid_step=8, pcg_iters=5, patch_iters=5, subdomain_px=16)),
     (3840, 2160, 4, SolveSchedule(levels=5, grid_step=4, gn_per_level=[1, 1, 2, 2, 2], pcg_iters=5,
                                   patch_iters=5, subdomain_px=16)),
+    (128, 96, 2, GSCHED),
+    (640, 480, 3, SolveSchedule(levels=4, grid_step=8, pcg_iters=5, subdomain_px=0)),
+    (3840, 2160, 4, SolveSchedule(levels=5, grid_step=4, gn_per_level=[1, 1, 2, 2, 2], pcg_iters=5,
+                                  subdomain_px=0)),
 ])
 def test_split_device_matches_unsplit_device(device, w, h, world, sched):
     imgs = _frames(w, h, seed=3)
@@ -138,7 +154,7 @@ def test_split_device_matches_unsplit_device(device, w, h, world, sched):
         r.close()
 
 
-def _nccl_worker(port: int, q):
+def _nccl_worker(port: int, q, mode: str = "schwarz"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch
     import torch.distributed as dist
@@ -149,7 +165,7 @@ def _nccl_worker(port: int, q):
         from paper_1610_07159_b200.hwflow import Solver
         from paper_1610_07159_b200.split import TorchComm
         solver = Solver(build.CUDA_LIB)
-        me = SplitRank(solver, 128, 96, DTYPE_U8, EnergyParams(), SCHED, None, 0, 1)
+        me = SplitRank(solver, 128, 96, DTYPE_U8, EnergyParams(), MODES[mode], None, 0, 1)
         ((r, st),) = solve_split([me], TorchComm(me), _frames())
         q.put((r.grid_total, r.vis4))
     finally:
@@ -157,11 +173,12 @@ def _nccl_worker(port: int, q):
 
 
 @pytest.mark.gpu
-def test_split_nccl_single_rank(device):
-    ref = _unsplit(device, _frames(), SCHED)
+@pytest.mark.parametrize("mode", ["schwarz", "global"])
+def test_split_nccl_single_rank(device, mode):
+    ref = _unsplit(device, _frames(), MODES[mode])
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    p = ctx.Process(target=_nccl_worker, args=(_free_port(), q))
+    p = ctx.Process(target=_nccl_worker, args=(_free_port(), q, mode))
     p.start()
     grid, vis = q.get(timeout=300)
     p.join(timeout=60)
