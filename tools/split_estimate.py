@@ -7,7 +7,7 @@ the script prints a projected N-GPU frame time: max over ranks of busy time, plu
 at an assumed NVLink rate and per-collective latency. This is an estimate, labelled as such. With
 one GPU per gpurun call, multi-GPU runs cannot be measured here.
 
-    python tools/split_estimate.py --worlds 1 2 4 8
+    python tools/split_estimate.py --worlds 1 2 4 8 [--mode global|schwarz]
 """
 from __future__ import annotations
 
@@ -55,6 +55,12 @@ class Timed(SplitRank):
     def sweep(self, l, s):
         self._t(super().sweep, l, s)
 
+    def pcg(self, l, phase, it=0):
+        self._t(super().pcg, l, phase, it)
+
+    def pcg_scalars(self, l, phase, it=0):
+        self._t(super().pcg_scalars, l, phase, it)
+
     def energy_after(self, l):
         self._t(super().energy_after, l)
 
@@ -73,15 +79,15 @@ class CountingComm(LocalComm):
         self.halos = self.gathers = 0
 
     def halo(self, ranks, level, name):
-        gw = ranks[0].rows[level][2]
-        self.halo_bytes += 2 * 6 * gw * 8  # one row each way per boundary, per rank (upper bound)
+        w = ranks[0].row_elems(level, name)
+        self.halo_bytes += 2 * w * 8  # one row each way per boundary, per rank (upper bound)
         self.halos += 1
         super().halo(ranks, level, name)
 
     def allgather_rows(self, ranks, level, name):
-        gw = ranks[0].rows[level][2]
+        w = ranks[0].row_elems(level, name)
         gh = max(r.rows[level][1] for r in ranks)
-        self.gather_bytes += 6 * gw * gh * 8  # every rank receives the whole grid
+        self.gather_bytes += w * gh * 8  # every rank receives the whole buffer
         self.gathers += 1
         super().allgather_rows(ranks, level, name)
 
@@ -90,10 +96,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--worlds", type=int, nargs="+", default=[1, 2, 4, 8])
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--mode", choices=["global", "schwarz"], default="global")
     a = ap.parse_args()
     dev = Solver(build.CUDA_LIB)
     imgs = synthetic.uhd_pair(0)[0]
-    S = SolveSchedule(levels=5, grid_step=4, pcg_iters=5, patch_iters=5, subdomain_px=16)
+    S = SolveSchedule(levels=5, grid_step=4, pcg_iters=5, patch_iters=5, subdomain_px=16 if a.mode == "schwarz" else 0)
     h, w = imgs.shape[1:]
     out = []
     for world in a.worlds:
@@ -105,7 +112,7 @@ def main():
         xfer_ms = (comm.halo_bytes + comm.gather_bytes) / (NVLINK_GBS * 1e9) * 1e3
         lat_ms = (comm.halos + comm.gathers) * LATENCY_US / 1e3 if world > 1 else 0.0
         proj = max(busy) + (xfer_ms + lat_ms if world > 1 else 0.0)
-        row = {"world": world, "rank_busy_ms": [round(b, 3) for b in busy], "max_busy_ms": round(max(busy), 3),
+        row = {"mode": a.mode, "world": world, "rank_busy_ms": [round(b, 3) for b in busy], "max_busy_ms": round(max(busy), 3),
                "exchanges": comm.halos + comm.gathers, "exchange_MB": round((comm.halo_bytes + comm.gather_bytes) / 1e6, 2),
                "projected_frame_ms": round(proj, 3), "projected_hz": round(1000.0 / proj, 1)}
         out.append(row)
