@@ -591,49 +591,78 @@ __device__ __forceinline__ double tile_spmv(const PcgArgs& a, const PcgPtr& P, c
                                             const double* __restrict__ p_prev, double* __restrict__ p_next,
                                             double (*ph)[6][kPhCols]) {
   const int j = threadIdx.x & 31;
-  const int span = 6 * (T.width + 2);  // rows b-1..b+1, nodes a0-1 .. a0+width
+  const bool act = j < T.width;
+  const int a_ = T.a0 + min(j, max(T.width - 1, 0));
+  const size_t n = static_cast<size_t>(T.b) * a.gw + a_;
+  // block s9 of this node's row: forward slots from its own record, backward ones as the
+  // neighbour's forward block; invalid slots read the own record (never used) so every load is
+  // unconditional and the next block's loads can be in flight during this block's FMAs
+  auto block = [&](int s9, bool& valid) -> const double* {
+    const int dx = s9 % 3 - 1, dy = s9 / 3 - 1;
+    const int qa = a_ + dx, qb = T.b + dy;
+    valid = act && qa >= 0 && qa < a.gw && qb >= 0 && qb < a.gh;
+    const size_t nq = s9 >= 4 || !valid ? n : static_cast<size_t>(qb) * a.gw + qa;
+    return P.sys + static_cast<size_t>(s9 >= 4 ? s9 - 4 : 4 - s9) * 21 * P.G + nq;
+  };
+  double A[2][21];
+  bool vb[9];
+  {
+    const double* b0 = block(0, vb[0]);
+#pragma unroll
+    for (int m = 0; m < 21; ++m) A[0][m] = __ldg(b0 + m * P.G);
+  }
+  // stage p_next = z + beta p_prev, rows b-1..b+1 x nodes a0-1 .. a0+width (6 (width + 2) contiguous
+  // doubles per row), all of a row's loads issued before its stores
+  const int span = 6 * (T.width + 2);
   __syncwarp();
+#pragma unroll
   for (int row = 0; row < 3; ++row) {
     const int qb = T.b - 1 + row;
-    for (int i = j; i < span; i += 32) {
-      const int col = i / 6, c = i - 6 * col, qa = T.a0 - 1 + col;
+    constexpr int kPer = (6 * (kPcgTile + 2) + 31) / 32;
+    double zz[kPer], pp[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int i = j + 32 * k, col = i / 6, c = i - 6 * col, qa = T.a0 - 1 + col;
+      const bool ok = i < span && qa >= 0 && qa < a.gw && qb >= 0 && qb < a.gh;
+      const size_t o = ok ? 6 * (static_cast<size_t>(qb) * a.gw + qa) + c : 0;
+      zz[k] = ok ? __ldcg(P.z + o) : 0.0;
+      pp[k] = ok ? __ldcg(p_prev + o) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int i = j + 32 * k, col = i / 6, c = i - 6 * col, qa = T.a0 - 1 + col;
+      if (i >= span) continue;
+      const bool ok = qa >= 0 && qa < a.gw && qb >= 0 && qb < a.gh;
       double v = 0.0;
-      if (qa >= 0 && qa < a.gw && qb >= 0 && qb < a.gh) {
-        const size_t o = 6 * (static_cast<size_t>(qb) * a.gw + qa) + c;
-        v = __ldcg(P.z + o) + beta * __ldcg(p_prev + o);  // p = z + beta p (solver.cpp:358)
+      if (ok) {
+        v = zz[k] + beta * pp[k];  // p = z + beta p (solver.cpp:358)
         // own row; in a strip split also the halo rows, which the neighbouring rank owns: the
         // same z + beta p from the exchanged z, so only z crosses ranks
         const bool keep = row == 1 || (row == 0 && T.b == a.row_lo && a.row_lo > 0) ||
                           (row == 2 && T.b == a.row_hi - 1 && a.row_hi < a.gh);
-        if (keep && col >= 1 && col <= T.width) p_next[o] = v;
+        if (keep && col >= 1 && col <= T.width) p_next[6 * (static_cast<size_t>(qb) * a.gw + qa) + c] = v;
       }
       ph[row][c][col] = v;
     }
   }
   __syncwarp();
-  const bool act = j < T.width;
-  const int a_ = T.a0 + min(j, max(T.width - 1, 0));
-  const size_t n = static_cast<size_t>(T.b) * a.gw + a_;
   double acc[6] = {0, 0, 0, 0, 0, 0};
 #pragma unroll
   for (int s9 = 0; s9 < 9; ++s9) {  // NormalSystem::apply (solver.cpp:80-98)
-    const int dx = s9 % 3 - 1, dy = s9 / 3 - 1;
-    const int qa = a_ + dx, qb = T.b + dy;
-    const bool valid = act && qa >= 0 && qa < a.gw && qb >= 0 && qb < a.gh;
-    if (!valid) continue;
-    // forward slots from this node's record, backward ones as the neighbour's forward block
-    const size_t nq = s9 >= 4 ? n : static_cast<size_t>(qb) * a.gw + qa;
-    const double* blk = P.sys + static_cast<size_t>(s9 >= 4 ? s9 - 4 : 4 - s9) * 21 * P.G + nq;
-    double A[21];
+    if (s9 + 1 < 9) {
+      const double* bn = block(s9 + 1, vb[s9 + 1]);
 #pragma unroll
-    for (int m = 0; m < 21; ++m) A[m] = __ldg(blk + m * P.G);
+      for (int m = 0; m < 21; ++m) A[(s9 + 1) & 1][m] = __ldg(bn + m * P.G);
+    }
+    if (!vb[s9]) continue;
+    const int dx = s9 % 3 - 1, dy = s9 / 3 - 1;
     double pv[6];
 #pragma unroll
     for (int c = 0; c < 6; ++c) pv[c] = ph[1 + dy][c][j + 1 + dx];
 #pragma unroll
     for (int i = 0; i < 6; ++i)
 #pragma unroll
-      for (int c = 0; c < 6; ++c) acc[i] += A[sym6(i, c)] * pv[c];
+      for (int c = 0; c < 6; ++c) acc[i] += A[s9 & 1][sym6(i, c)] * pv[c];
   }
   double pown[6];
 #pragma unroll
@@ -745,7 +774,7 @@ __global__ void __launch_bounds__(kPcgThreads) k_pcg_init(const PcgArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(kPcgThreads) k_pcg_spmv(const PcgArgs a, int it) {
+__global__ void __launch_bounds__(kPcgThreads, 4) k_pcg_spmv(const PcgArgs a, int it) {
   __shared__ double ph_all[kPcgWarps][3][6][kPhCols];
   __shared__ double red[kPcgWarps];
   __shared__ int sflag;
