@@ -114,7 +114,8 @@ def extra_configs(dev, lib, h, C, capi, reps: int = 5) -> dict:
     # live sequences, each step warm-started from the previous frame's device-resident
     # hierarchy (hwf_solve_batch_seq; states ping-pong), 16 parallel sequences of 640x480, host in/out; global
     # PCG (the reference's Schwarz mode diverges on these noise-free constant-velocity scenes, as in the tests)
-    nseq, steps = 16, 3
+    # (frames 0 and 1 are untimed: the cold start and the first warm start build their plans)
+    nseq, steps = 16, 6
     per_seq = [synthetic.sequence_pairs(steps, W_, H_, seed=1610 + i) for i in range(nseq)]
     frames = [np.ascontiguousarray(np.stack([per_seq[i][k] for i in range(nseq)])) for k in range(steps)]
     if True:
@@ -123,11 +124,12 @@ def extra_configs(dev, lib, h, C, capi, reps: int = 5) -> dict:
         status = "ok"
         try:
             dev.solve_batch_seq(frames[0], EnergyParams(), S, None, st[0], outputs=("grid_total",))
+            dev.solve_batch_seq(frames[1], EnergyParams(), S, st[0], st[1], outputs=("grid_total",))
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            for k in range(1, len(frames)):
+            for k in range(2, len(frames)):
                 dev.solve_batch_seq(frames[k], EnergyParams(), S, st[(k - 1) % 2], st[k % 2], outputs=("grid_total",))
-            dt = (time.perf_counter() - t0) / (len(frames) - 1)
+            dt = (time.perf_counter() - t0) / (len(frames) - 2)
         except capi.SolverDivergence:
             status, dt = "diverged-flag", float("nan")
         out["cfg2_sequence_warm_start_global_pcg_16x"] = {"pairs": nseq, "ms_per_step": 1000.0 * dt,
@@ -402,6 +404,7 @@ def run_ours(args, ws, rank, local):
     flow_err = synthetic.flow_error(host_grid[(args.steps - 1) % 2].numpy(),
                                     [synthetic.webcam_truth(i) for i in range(pairs.start, pairs.start + B)])
     gn_total = sum(S.gn_for_level(l) for l in range(4))
+    lib.hwf_set_profiling(h, 0)  # the side measurements build their own plans, without timing events
     extra = extra_configs(dev, lib, h, C, capi) if (rank == 0 and ws == 1 and not args.no_extra) else None
     if rank == 0:
         cb = cpu_baseline(max(1, min(3, args.steps)), 1, args.mode) if ws == 1 and not args.no_cpu else None
