@@ -70,8 +70,7 @@ struct LevelDev {
   int w = 0, h = 0, gw = 0, gh = 0, step = 0, ncx = 0, ncy = 0, tcx = 0, tcy = 0, rp = 0;
   int ntx = 0, nty = 0, nxm = 0, nym = 0, tile = 0;
   size_t N = 0, G = 0, C = 0;
-  double2* pk = nullptr;
-  double* gy = nullptr;
+  double* pk = nullptr;  // 32 B sample texels (k_pack)
   double *img = nullptr, *illum = nullptr, *base = nullptr, *delta = nullptr, *total = nullptr;
   double *nodew = nullptr, *nodew2 = nullptr, *nodew_a = nullptr, *nodew_b = nullptr, *half = nullptr, *cells = nullptr, *sys = nullptr, *xa = nullptr, *xb = nullptr,
          *hm = nullptr;
@@ -200,7 +199,7 @@ inline PixArgs pixel_args(const LevelDev& d, const hwf_energy_params& P, const h
   PixArgs pa{};
   pa.w = d.w; pa.h = d.h; pa.gw = d.gw; pa.gh = d.gh; pa.step = d.step; pa.ncx = d.ncx; pa.ncy = d.ncy;
   pa.tcx = d.tcx; pa.tcy = d.tcy; pa.rp = d.rp;
-  pa.pk = d.pk; pa.gy = d.gy; pa.src8 = src8; pa.illum = d.illum; pa.vis4 = d.vis; pa.W = d.W;
+  pa.pk = d.pk; pa.src8 = src8; pa.illum = d.illum; pa.vis4 = d.vis; pa.W = d.W;
   pa.hmc = d.hmc; pa.wc = d.wc; pa.hc = d.hc;
   pa.total = d.total; pa.half = d.half; pa.cells = d.cells; pa.ep_pair = E.pair_stride(); pa.flags = flags;
   pa.P = to_params(P); pa.active = S.active_fields;
@@ -472,8 +471,7 @@ struct Plan {
       LevelDev& d = lv[l];
       if (!u8_finest(l)) {
         d.img = mem.alloc<double>(B * 4 * d.N);
-        d.pk = mem.alloc<double2>(B * 4 * d.N);
-        d.gy = mem.alloc<double>(B * 4 * d.N);
+        d.pk = mem.alloc<double>(B * 4 * d.N * 4);
       }
       d.alloc_solver(mem, B, S.subdomain_px > 0);
       d.occ = mem.alloc<uint8_t>(B * d.N);
@@ -562,7 +560,7 @@ struct Plan {
     }
     for (int l = 0; l < L; ++l) {
       if (u8_finest(l)) continue;
-      launch_pack(lv[l].img, lv[l].w, lv[l].h, 4 * B, lv[l].pk, lv[l].gy, st);
+      launch_pack(lv[l].img, lv[l].w, lv[l].h, 4 * B, lv[l].pk, st);
       LC.count++;
     }
   }

@@ -19,8 +19,7 @@ enum : int {
 
 struct PixArgs {
   int w, h, gw, gh, step, ncx, ncy, tcx, tcy, rp;
-  const double2* pk;    // [B][4][N] {value, grad x} (k_pack)
-  const double* gy;     // [B][4][N] grad y (k_pack)
+  const double* pk;     // [B][4][N][4] {value, grad x, grad y, 0} (k_pack): 32 B texels, one 256-bit load each
   const uint8_t* src8;  // [B][4][N] u8 frames of the finest level (then pk/gy unused), or null
   const double* illum;  // [B][4][N] or null (stage seams: explicit maps)
   // pipeline: the coarser level's half maps [B][2][wc*hc]; illum of image e at (x, y) is
@@ -119,7 +118,7 @@ int pixel_tile_cells_y(int step);
 int pixel_smem_pitch(int step);
 size_t pixel_smem_bytes(int step);
 void launch_pixel(bool lin, const PixArgs& a, int B, cudaStream_t s);
-void launch_pack(const double* img, int w, int h, int planes, double2* pk, double* gy, cudaStream_t s);
+void launch_pack(const double* img, int w, int h, int planes, double* pk, cudaStream_t s);
 int node_ctas(int G);
 void launch_node(bool lin, const NodeArgs& a, int B, cudaStream_t s);
 void launch_structw(int w, int h, int gw, int gh, int step, const double* half, double* wout, int B,

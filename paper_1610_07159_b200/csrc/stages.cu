@@ -33,9 +33,8 @@ void load_level(DevMem& m, LevelDev& d, const hwf_level* lv, bool schwarz_tiles,
     if (!lv->images[e]) throw InvalidArg("null image");
     CK(cudaMemcpy(d.img + e * d.N, lv->images[e], d.N * sizeof(double), cudaMemcpyHostToDevice));
   }
-  d.pk = m.alloc<double2>(4 * d.N);
-  d.gy = m.alloc<double>(4 * d.N);
-  launch_pack(d.img, d.w, d.h, 4, d.pk, d.gy, st);
+  d.pk = m.alloc<double>(4 * d.N * 4);
+  launch_pack(d.img, d.w, d.h, 4, d.pk, st);
   bool any = false;
   for (int e = 0; e < 4; ++e) any = any || lv->illum[e];
   if (any) {
@@ -74,7 +73,7 @@ PixArgs pix_args(const LevelDev& d, const hwf_energy_params* P, uint32_t active,
   PixArgs pa{};
   pa.w = d.w; pa.h = d.h; pa.gw = d.gw; pa.gh = d.gh; pa.step = d.step; pa.ncx = d.ncx; pa.ncy = d.ncy;
   pa.tcx = d.tcx; pa.tcy = d.tcy; pa.rp = d.rp;
-  pa.pk = d.pk; pa.gy = d.gy; pa.illum = d.illum; pa.vis4 = d.vis; pa.W = d.W; pa.total = d.total; pa.half = d.half;
+  pa.pk = d.pk; pa.illum = d.illum; pa.vis4 = d.vis; pa.W = d.W; pa.total = d.total; pa.half = d.half;
   pa.cells = d.cells; pa.ep_pair = E.pair_stride(); pa.flags = flags; pa.P = to_params(*P);
   pa.active = active; pa.ep_new = E.slot(0);
   return pa;
