@@ -317,24 +317,34 @@ __global__ void k_occ_resolve(int w, int h, const int2* __restrict__ q, const fl
   };
   const unsigned inc[6] = {cell_id(px, py, 0), cell_id(px - 1, py, 0), cell_id(px, py - 1, 0),
                             cell_id(px - 1, py, 1), cell_id(px - 1, py - 1, 1), cell_id(px, py - 1, 1)};
+  // all four views' loads first (vertex, then its z-buffer key), decisions after: the eight
+  // dependent loads overlap instead of running view by view
+  const bool inner = px < w - 1 && py < h - 1;
+  int2 qq[4];
+  bool dg[4];
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    bool v = !b;
-    if (v && px < w - 1 && py < h - 1 && degen[(static_cast<size_t>(pair) * 4 + e) * N + pix]) v = false;
-    if (v) {
-      const int2 qq = q[(static_cast<size_t>(pair) * 4 + e) * N + pix];
-      const long long rx = (static_cast<long long>(qq.x) + 128) >> 8, ry = (static_cast<long long>(qq.y) + 128) >> 8;
-      if (rx >= 0 && rx < w && ry >= 0 && ry < h) {
-        const unsigned long long key = zbuf[(static_cast<size_t>(pair) * 4 + e) * N + ry * w + rx];
-        if (key != ~0ULL) {
-          const unsigned int tri = static_cast<unsigned int>(key & 0xffffffffULL);
-          const bool ring = tri == inc[0] || tri == inc[1] || tri == inc[2] || tri == inc[3] ||
-                            tri == inc[4] || tri == inc[5];
-          if (!ring) {
-            const float zf = __uint_as_float(static_cast<unsigned int>(key >> 32));
-            if (__dadd_rn(zown, -kDepthTol) > static_cast<double>(zf)) v = false;
-          }
-        }
+    const size_t o = (static_cast<size_t>(pair) * 4 + e) * N + pix;
+    qq[e] = q[o];
+    dg[e] = inner && degen[o];
+  }
+  unsigned long long key[4];
+  bool inr[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const long long rx = (static_cast<long long>(qq[e].x) + 128) >> 8, ry = (static_cast<long long>(qq[e].y) + 128) >> 8;
+    inr[e] = rx >= 0 && rx < w && ry >= 0 && ry < h;
+    key[e] = zbuf[(static_cast<size_t>(pair) * 4 + e) * N + (inr[e] ? ry * w + rx : 0)];
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    bool v = !b && !dg[e];
+    if (v && inr[e] && key[e] != ~0ULL) {
+      const unsigned int tri = static_cast<unsigned int>(key[e] & 0xffffffffULL);
+      const bool ring = tri == inc[0] || tri == inc[1] || tri == inc[2] || tri == inc[3] || tri == inc[4] || tri == inc[5];
+      if (!ring) {
+        const float zf = __uint_as_float(static_cast<unsigned int>(key[e] >> 32));
+        if (__dadd_rn(zown, -kDepthTol) > static_cast<double>(zf)) v = false;
       }
     }
     if (v) bits |= static_cast<uint8_t>(1u << e);
