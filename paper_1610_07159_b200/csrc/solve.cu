@@ -543,15 +543,24 @@ __device__ __forceinline__ void st6(double* p, const double (&v)[6]) {
 }
 
 // z = M r (solver.cpp:468-474 via NormalSystem::precond_block): the node's three 2x2 blocks
-__device__ __forceinline__ void pcg_precond(const PcgPtr& P, size_t n, const double (&r)[6], double (&z)[6]) {
+// (split in two so callers can issue the nine loads before their stores: the compiler cannot move
+// them across stores it cannot prove disjoint)
+__device__ __forceinline__ void pcg_precond_load(const PcgPtr& P, size_t n, double (&M)[9]) {
+#pragma unroll
+  for (int i = 0; i < 9; ++i) M[i] = __ldg(P.sys + (kSysPre + i) * P.G + n);
+}
+__device__ __forceinline__ void pcg_precond_apply(const double (&M)[9], const double (&r)[6], double (&z)[6]) {
 #pragma unroll
   for (int f = 0; f < 3; ++f) {
-    const double m0 = __ldg(P.sys + (kSysPre + 3 * f) * P.G + n);
-    const double m1 = __ldg(P.sys + (kSysPre + 3 * f + 1) * P.G + n);
-    const double m2 = __ldg(P.sys + (kSysPre + 3 * f + 2) * P.G + n);
+    const double m0 = M[3 * f], m1 = M[3 * f + 1], m2 = M[3 * f + 2];
     z[2 * f] = m0 * r[2 * f] + m1 * r[2 * f + 1];
     z[2 * f + 1] = m1 * r[2 * f] + m2 * r[2 * f + 1];
   }
+}
+__device__ __forceinline__ void pcg_precond(const PcgPtr& P, size_t n, const double (&r)[6], double (&z)[6]) {
+  double M[9];
+  pcg_precond_load(P, n, M);
+  pcg_precond_apply(M, r, z);
 }
 
 // Tile partial of one per-node value (xor tree over the warp); every lane returns it.
@@ -676,7 +685,8 @@ __device__ __forceinline__ void tile_update(const PcgArgs& a, const PcgPtr& P, c
   const int j = threadIdx.x & 31;
   const bool act = j < T.width;
   const size_t n = tile_node(a, T, j);
-  double r[6] = {0, 0, 0, 0, 0, 0}, z[6];
+  double r[6] = {0, 0, 0, 0, 0, 0}, z[6], M[9];
+  pcg_precond_load(P, n, M);
   if (act) {
     double x[6], p[6], ap[6];
     ld6(P.x + 6 * n, x);
@@ -691,7 +701,7 @@ __device__ __forceinline__ void tile_update(const PcgArgs& a, const PcgPtr& P, c
     st6(P.x + 6 * n, x);
     st6(P.r + 6 * n, r);
   }
-  pcg_precond(P, n, r, z);
+  pcg_precond_apply(M, r, z);
   if (act) st6(P.z + 6 * n, z);
   prz = tile_partial(act, node_dot(r, z));
   prr = want_rr ? tile_partial(act, node_dot(r, r)) : 0.0;
