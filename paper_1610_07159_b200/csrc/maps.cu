@@ -245,10 +245,20 @@ __global__ void k_occ_raster(int w, int h, const int2* __restrict__ q, const flo
   const bool bad0 = b00 || b10 || b01, bad1 = b10 || b11 || b01;
   const float zf0 = fminf(z00, fminf(z10, z01)), zf1 = fminf(z10, fminf(z11, z01));  // flat depth per triangle
   const unsigned int tri0 = static_cast<unsigned int>(2 * (cy * cw + cx));
+  // view e + 1's vertices load while view e rasterises (the compiler cannot move them above the
+  // z-buffer atomics itself)
+  const int2* Q0 = q + static_cast<size_t>(pair) * 4 * N;
+  int2 n00 = Q0[i00], n10 = Q0[i10], n01 = Q0[i01], n11 = Q0[i11];
 #pragma unroll 1
   for (int e = 0; e < 4; ++e) {  // the 4 views share the cell's depth and validity
-    const int2* Q = q + (static_cast<size_t>(pair) * 4 + e) * N;
-    const int2 p00 = Q[i00], p10 = Q[i10], p01 = Q[i01], p11 = Q[i11];
+    const int2 p00 = n00, p10 = n10, p01 = n01, p11 = n11;
+    if (e < 3) {
+      const int2* Qn = q + (static_cast<size_t>(pair) * 4 + e + 1) * N;
+      n00 = Qn[i00];
+      n10 = Qn[i10];
+      n01 = Qn[i01];
+      n11 = Qn[i11];
+    }
     unsigned long long* zb = zbuf + (static_cast<size_t>(pair) * 4 + e) * N;
     const unsigned long long qtag =
         (static_cast<unsigned long long>(pair) << 34) | (static_cast<unsigned long long>(e) << 32);
