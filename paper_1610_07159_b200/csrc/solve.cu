@@ -642,19 +642,26 @@ __device__ __forceinline__ double tile_spmv(const PcgArgs& a, const PcgPtr& P, c
       const int i = j + 32 * k, col = i / 6, c = i - 6 * col, qa = T.a0 - 1 + col;
       if (i >= span) continue;
       const bool ok = qa >= 0 && qa < a.gw && qb >= 0 && qb < a.gh;
-      double v = 0.0;
-      if (ok) {
-        v = zz[k] + beta * pp[k];  // p = z + beta p (solver.cpp:358)
-        // own row; in a strip split also the halo rows, which the neighbouring rank owns: the
-        // same z + beta p from the exchanged z, so only z crosses ranks
-        const bool keep = row == 1 || (row == 0 && T.b == a.row_lo && a.row_lo > 0) ||
-                          (row == 2 && T.b == a.row_hi - 1 && a.row_hi < a.gh);
-        if (keep && col >= 1 && col <= T.width) p_next[6 * (static_cast<size_t>(qb) * a.gw + qa) + c] = v;
-      }
+      const double v = ok ? zz[k] + beta * pp[k] : 0.0;  // p = z + beta p (solver.cpp:358)
       ph[row][c][col] = v;
     }
   }
   __syncwarp();
+  // p_next to global only now, from shared memory: global stores inside the staging would keep the
+  // compiler from hoisting the later rows' loads. The own row; in a strip split also the halo rows,
+  // which the neighbouring rank owns (the same z + beta p from the exchanged z, so only z crosses ranks).
+  if (act) {
+#pragma unroll
+    for (int row = 0; row < 3; ++row) {
+      const bool keep = row == 1 || (row == 0 && T.b == a.row_lo && a.row_lo > 0) ||
+                        (row == 2 && T.b == a.row_hi - 1 && a.row_hi < a.gh);
+      if (!keep) continue;
+      double pr[6];
+#pragma unroll
+      for (int c = 0; c < 6; ++c) pr[c] = ph[row][c][j + 1];
+      st6(p_next + 6 * (n + static_cast<long long>(row - 1) * a.gw), pr);
+    }
+  }
   double acc[6] = {0, 0, 0, 0, 0, 0};
 #pragma unroll
   for (int s9 = 0; s9 < 9; ++s9) {  // NormalSystem::apply (solver.cpp:80-98)
