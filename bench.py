@@ -449,7 +449,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--batch", type=int, default=128, help="frame pairs per GPU per step")
+    ap.add_argument("--batch", type=int, default=256,
+                    help="frame pairs per GPU per step (256 = BASELINE cfg4's pair count at N = 1)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--mode", choices=["schwarz", "global"], default="global")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
