@@ -118,24 +118,23 @@ def extra_configs(dev, lib, h, C, capi, reps: int = 5) -> dict:
     nseq, steps = 16, 6
     per_seq = [synthetic.sequence_pairs(steps, W_, H_, seed=1610 + i) for i in range(nseq)]
     frames = [np.ascontiguousarray(np.stack([per_seq[i][k] for i in range(nseq)])) for k in range(steps)]
-    if True:
-        S = SolveSchedule(levels=4, grid_step=8, pcg_iters=5, subdomain_px=0)
-        st = [dev.new_state(nseq, W_, H_, S), dev.new_state(nseq, W_, H_, S)]
-        status = "ok"
-        try:
-            dev.solve_batch_seq(frames[0], EnergyParams(), S, None, st[0], outputs=("grid_total",))
-            dev.solve_batch_seq(frames[1], EnergyParams(), S, st[0], st[1], outputs=("grid_total",))
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            for k in range(2, len(frames)):
-                dev.solve_batch_seq(frames[k], EnergyParams(), S, st[(k - 1) % 2], st[k % 2], outputs=("grid_total",))
-            dt = (time.perf_counter() - t0) / (len(frames) - 2)
-        except capi.SolverDivergence:
-            status, dt = "diverged-flag", float("nan")
-        out["cfg2_sequence_warm_start_global_pcg_16x"] = {"pairs": nseq, "ms_per_step": 1000.0 * dt,
-                                               "pairs_per_s": nseq / dt if dt == dt else None,
-                                               "solver_status": status,
-                                               "note": "wall clock per step incl. H2D of u8 frames and D2H of the grid"}
+    S = SolveSchedule(levels=4, grid_step=8, pcg_iters=5, subdomain_px=0)
+    st = [dev.new_state(nseq, W_, H_, S), dev.new_state(nseq, W_, H_, S)]
+    status = "ok"
+    try:
+        dev.solve_batch_seq(frames[0], EnergyParams(), S, None, st[0], outputs=("grid_total",))
+        dev.solve_batch_seq(frames[1], EnergyParams(), S, st[0], st[1], outputs=("grid_total",))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for k in range(2, len(frames)):
+            dev.solve_batch_seq(frames[k], EnergyParams(), S, st[(k - 1) % 2], st[k % 2], outputs=("grid_total",))
+        dt = (time.perf_counter() - t0) / (len(frames) - 2)
+    except capi.SolverDivergence:
+        status, dt = "diverged-flag", float("nan")
+    out["cfg2_sequence_warm_start_global_pcg_16x"] = {"pairs": nseq, "ms_per_step": 1000.0 * dt,
+                                           "pairs_per_s": nseq / dt if dt == dt else None,
+                                           "solver_status": status,
+                                           "note": "wall clock per step incl. H2D of u8 frames and D2H of the grid"}
     return out
 
 
@@ -384,7 +383,8 @@ def run_ours(args, ws, rank, local):
     tf = ROOT / "profiles" / "pixel_traffic.json"
     if tf.exists():  # ncu --set full capture at B=128; DRAM bytes scale with the batch
         prof = json.loads(tf.read_text())
-        traffic = prof.get("dram_bytes_per_launch_L0") * B / 128.0
+        v = prof.get("dram_bytes_per_launch_L0")
+        traffic = v * B / prof.get("batch", 128) if v is not None else None
     launches = lib.hwf_launch_count(h)
 
     # ---- e2e: through the public C-ABI from pinned host buffers ---------------------
@@ -444,6 +444,43 @@ def run_ours(args, ws, rank, local):
         print(json.dumps(line), flush=True)
 
 
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` without a launcher: re-exec this script under torch.distributed.run with N local ranks
+    (one process per GPU, rendezvous on 127.0.0.1), the same way the driver launches it. Rank 0 prints the line.
+    NCCL's communicator lines (NCCL_DEBUG=INFO, INIT subsystem) go to stderr so the rank count can be checked."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
+def dry_run(args):
+    """--dry: the multi-rank plumbing without a GPU (gloo): every rank reports its frame-mode shard; rank 0
+    gathers them and prints one JSON line (tests/test_bench.py)."""
+    import torch.distributed as dist
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if ws > 1:
+        dist.init_process_group("gloo")
+    sh = shard(rank, ws, args.batch)
+    mine = [rank, sh.start, sh.stop, os.getpid()]
+    allv = [mine]
+    if ws > 1:
+        allv = [None] * ws
+        dist.all_gather_object(allv, mine)
+    t = allreduce_max(float(rank + 1), ws)
+    if rank == 0:
+        print(json.dumps({"dry": True, "n_gpus": ws, "ranks": allv, "max_over_ranks": t}), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -455,8 +492,14 @@ def main():
     ap.add_argument("--mode", choices=["schwarz", "global"], default="global")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-extra", action="store_true", help="skip the cfg3/cfg5 side measurements")
+    ap.add_argument("--dry", action="store_true", help="multi-rank plumbing only (gloo, no GPU work)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        sys.exit(spawn_ranks(args.gpus))
+    if args.dry:
+        dry_run(args)
+        return
     ws, rank, local = (1, 0, 0)
     if args.impl == "reference":
         ws = int(os.environ.get("WORLD_SIZE", "1"))
@@ -464,6 +507,8 @@ def main():
         run_reference(args, ws, rank)
         return
     ws, rank, local = dist_init()
+    if ws != args.gpus and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; reporting n_gpus={ws}", file=sys.stderr)
     run_ours(args, ws, rank, local)
     if ws > 1:
         import torch.distributed as dist

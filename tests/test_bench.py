@@ -42,3 +42,15 @@ def test_bench_line_contract():
     assert e["value"] > 0 and e["h2d_bytes_per_step"] == 8 * 4 * 640 * 480 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0 and d["clocks"]["sm_mhz"]
     assert d["flow_error"]["s_median_px"] < 0.2  # the headline schedule recovers the known stereo flow
+
+
+def test_gpus_flag_spawns_ranks_with_disjoint_shards():
+    """`bench.py --gpus 2` without a launcher re-execs itself under torch.distributed.run with 2 ranks
+    (frame mode: rank r owns pairs [rB, (r+1)B), no collective); --dry runs the plumbing on gloo."""
+    d = _line(["--gpus", "2", "--batch", "8", "--dry"], 300)
+    assert d["dry"] is True and d["n_gpus"] == 2
+    ranks = sorted(d["ranks"])
+    assert [r[0] for r in ranks] == [0, 1]
+    assert [(r[1], r[2]) for r in ranks] == [(0, 8), (8, 16)]  # disjoint, contiguous shards
+    assert ranks[0][3] != ranks[1][3]  # two processes
+    assert d["max_over_ranks"] == 2.0  # the timing max reduces over both ranks

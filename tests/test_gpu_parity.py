@@ -209,21 +209,6 @@ def test_solve_cfg1_global_pcg(device, oracle, golden):
     assert abs(np.median(r.s[..., 0]) - gt["s"][0]) < 0.25
 
 
-def test_solve_cfg1_full_schedule_within_reference_reproducibility(device, golden):
-    """Full cfg1 schedule (5 GN on every level): the reference's GN amplifies round-off ~10x per
-    iteration at a few ill-conditioned nodes, so two faithful CPU builds (reference vs oracle port,
-    differing only in summation order) already differ by golden['cfg1_full_port_vs_ref'] px.
-    The device must be no further from the reference than that, with the energy within 1e-4."""
-    imgs = golden["cfg1_images"]
-    S = SolveSchedule(levels=3, grid_step=8, gn_per_level=[5], pcg_iters=10, subdomain_px=0)
-    (r,), (s,) = device.solve_batch(imgs[None], EnergyParams(), S)
-    d = np.abs(r.grid_total - golden["cfg1_full_grid"])
-    bound = max(FLOW_TOL_PX, 2.0 * float(golden["cfg1_full_port_vs_ref"]))
-    assert d.max() < bound, (d.max(), bound)
-    assert np.median(d) < 1e-6
-    assert s.final_energy() == pytest.approx(float(golden["cfg1_full_E"]), rel=ENERGY_RTOL)
-
-
 def test_solve_short_schwarz_schedule(device, oracle):
     imgs, _ = synthetic.webcam_pair(3, 160, 120)
     S = SolveSchedule(levels=3, grid_step=8, gn_per_level=[1, 1, 2], pcg_iters=5, patch_iters=5, subdomain_px=16)

@@ -327,3 +327,57 @@ def test_reference_schwarz_diverges_on_2x2_node_subdomains(oracle, reference):
         assert st.energy_after[0][-1] > 10 * st.energy_before[0][0]
     _, st = oracle.run_scene_flow(imgs, EnergyParams(), SolveSchedule(levels=2, grid_step=8, subdomain_px=0))
     assert st.energy_after[0][-1] < st.energy_before[0][0]
+
+
+# ---- the bench schedules: the port against the reference build, in lock step and end to end -------
+def test_port_lockstep_matches_reference_full_cfg1(oracle, reference):
+    """Every GN iteration of the full cfg1 schedule (3 levels x 5 GN x 10 PCG), both handed the reference's
+    state (tests/lockstep.py): one iteration of the port reproduces one of the reference within 1e-12 px,
+    bit-exact W, and bit-exact occlusion on the same flows. (Free-running, the two part by 9e-3 px after
+    15 iterations: the reference's GN amplifies one-ulp differences ~1e12; see test below.)"""
+    from lockstep import lockstep
+    imgs = synthetic.constant_pair(320, 240)[0]
+    S = SolveSchedule(levels=3, grid_step=8, gn_per_level=[5], pcg_iters=10, subdomain_px=0, threads=8)
+
+    def on_iter(l, it, A, B, ea, eb):
+        assert np.abs(A.delta - B.delta).max() < 1e-12, (l, it)
+        assert np.array_equal(A.W, B.W)
+        np.testing.assert_allclose(B.nw, A.nw, rtol=1e-12)
+        assert eb[1] == pytest.approx(ea[1], rel=1e-12)
+
+    def on_level(l, A, B):
+        assert np.array_equal(A.vis_prev, B.vis_prev)
+
+    lockstep(reference, oracle, imgs, S, EnergyParams(), sync=True, on_iter=on_iter, on_level=on_level)
+
+
+def test_reference_not_reproducible_to_1e3_on_full_cfg1(reference):
+    """Root cause of the end-to-end gap at BASELINE configs[0]: the reference against ITSELF with a one-ulp
+    change of a random half of its input pixels ends up to ~9e-3 px away (the golden envelope), while the
+    same experiment on the headline cfg2 schedule stays below 1e-5 px."""
+    from pathlib import Path
+    g = dict(np.load(Path(__file__).parent / "golden" / "ref_headline.npz"))
+    assert g["cfg1_full_draw_stats"][:, 0].max() > 1e-3  # ill-conditioned schedule
+    imgs = synthetic.webcam_pair(0)[0]
+    import bench
+    S = bench.schedule("global")
+    S.threads = 8
+    r0, _ = reference.run_scene_flow(imgs, EnergyParams(), S)
+    rng = np.random.default_rng(0)
+    f = imgs.astype(np.float64) / 255.0
+    r1, _ = reference.run_scene_flow(np.where(rng.random(f.shape) < 0.5, np.nextafter(f, 2.0), f), EnergyParams(), S)
+    assert np.abs(r1.grid_total - r0.grid_total).max() < 1e-4  # well-conditioned headline schedule
+    assert np.abs(r0.grid_total - g["cfg2_0_grid"]).max() == 0.0  # golden reproducible bit for bit
+
+
+def test_port_matches_reference_headline_golden(oracle):
+    """The oracle port at bench.py's cfg2 schedule against the reference-build golden (both CPU)."""
+    from pathlib import Path
+    g = dict(np.load(Path(__file__).parent / "golden" / "ref_headline.npz"))
+    import bench
+    S = bench.schedule("global")
+    S.threads = 8
+    imgs = synthetic.webcam_pair(2)[0]
+    q, _ = oracle.run_scene_flow(imgs, EnergyParams(), S)
+    assert np.abs(q.grid_total - g["cfg2_2_grid"]).max() < 1e-5
+    assert np.array_equal(q.vis4, g["cfg2_2_vis4"])
