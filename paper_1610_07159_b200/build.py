@@ -45,16 +45,21 @@ def _stale(target: Path, deps: list[Path]) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build_cuda(force: bool = False, verbose: bool = False) -> Path:
-    objdir = LIBDIR / "obj"
+def build_cuda(force: bool = False, verbose: bool = False, defines: tuple[str, ...] = (),
+               variant: str | None = None) -> Path:
+    """The product library; with `defines` (e.g. ("HWF_PIX_MINB=3",)) an A/B variant built to
+    lib/variants/<variant>/libhwflow_cuda.so (tools/ab.py)."""
+    objdir = LIBDIR / "obj" if variant is None else LIBDIR / "variants" / variant / "obj"
+    out = CUDA_LIB if variant is None else LIBDIR / "variants" / variant / "libhwflow_cuda.so"
     objdir.mkdir(parents=True, exist_ok=True)
+    dflags = [f"-D{d}" for d in defines]
     headers = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + list((ROOT / "include").glob("*.h"))
     nvcc = _nvcc()
 
     def compile_one(src: str) -> Path:
         obj = objdir / (Path(src).stem + ".o")
         if force or _stale(obj, [CSRC / src] + headers):
-            cmd = [nvcc, *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+            cmd = [nvcc, *NVCC_FLAGS, *dflags, "-c", str(CSRC / src), "-o", str(obj)]
             if verbose:
                 print(" ".join(cmd), flush=True)
             subprocess.run(cmd, check=True)
@@ -62,12 +67,12 @@ def build_cuda(force: bool = False, verbose: bool = False) -> Path:
 
     with cf.ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
-    if force or _stale(CUDA_LIB, objs):
-        cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", str(CUDA_LIB), *map(str, objs)]
+    if force or _stale(out, objs):
+        cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", str(out), *map(str, objs)]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
-    return CUDA_LIB
+    return out
 
 
 def build_oracle() -> None:

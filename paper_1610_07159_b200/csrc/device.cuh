@@ -194,10 +194,18 @@ __device__ __forceinline__ double2 pixel_grad(const double* __restrict__ I, int 
   return g;
 }
 
+// x / step (warp_grid.cpp:44-45), correctly rounded. A power-of-two step (every BASELINE config) is an exact
+// multiplication by 2^-k, the same double as the division, without the FP64 division sequence.
+__device__ __forceinline__ double div_step(double x, int step) {
+  if ((step & (step - 1)) == 0)
+    return x * __longlong_as_double(static_cast<long long>(1023 - (__ffs(step) - 1)) << 52);
+  return x / step;
+}
+
 // warp_grid.cpp:41-54 support for an in-coverage position; returns the cell.
 __device__ __forceinline__ void grid_support(int gw, int gh, int step, double x, double y, int& a0,
                                              int& b0, double& fu, double& fv) {
-  const double u = x / step, v = y / step;
+  const double u = div_step(x, step), v = div_step(y, step);
   a0 = min(max(static_cast<int>(floor(u)), 0), gw - 2);
   b0 = min(max(static_cast<int>(floor(v)), 0), gh - 2);
   fu = fmin(fmax(u - a0, 0.0), 1.0);

@@ -92,7 +92,7 @@ struct LevelDev {
     C = static_cast<size_t>(ncx) * ncy;
     tcx = pixel_tile_cells_x(step);
     tcy = pixel_tile_cells_y(step);
-    rp = pixel_smem_pitch(step);
+    rp = pixel_tile_pixels(w, h, step);  // k_pixel: product records per tile
     n_pix_cta = ((ncx + tcx - 1) / tcx) * ((ncy + tcy - 1) / tcy);
     n_node_cta = node_ctas(static_cast<int>(G));
     tile = tile_px;

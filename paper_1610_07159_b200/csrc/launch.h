@@ -115,8 +115,8 @@ void init_maps_constants();
 // pixel.cu
 int pixel_tile_cells_x(int step);
 int pixel_tile_cells_y(int step);
-int pixel_smem_pitch(int step);
-size_t pixel_smem_bytes(int step);
+int pixel_tile_pixels(int w, int h, int step);
+size_t pixel_smem_bytes(int tile_pixels, int step);
 void launch_pixel(bool lin, const PixArgs& a, int B, cudaStream_t s);
 void launch_pack(const double* img, int w, int h, int planes, double* pk, cudaStream_t s);
 int node_ctas(int G);

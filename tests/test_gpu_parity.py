@@ -259,9 +259,11 @@ def test_batch_is_bitwise_independent(device, sub):
 
 
 @pytest.mark.parametrize("w,h", [(128, 96), (131, 97)])
-def test_u8_finest_level_matches_f64_frames_bitwise(device, w, h):
-    """The finest level of u8 frames is sampled from the bytes (k/255 rebuilt in registers); it must be
-    bitwise identical to the packed-plane path that f64 frames k/255 take (k_pyr_in, k_pack)."""
+def test_u8_finest_level_matches_f64_frames(device, w, h):
+    """The finest level of u8 frames is sampled from the bytes in the integer domain (k_pixel<*, U8>); the f64
+    path samples the correctly rounded k/255 planes (k_pyr_in, k_pack). The two differ only by the rounding of
+    the interpolation (a few ulps per sample), so the solves agree to round-off: grids within 1e-9 px, masks
+    bit-exact, energies within 1e-12 relative."""
     frames = np.stack([synthetic.webcam_pair(i, w, h)[0] for i in range(2)])
     frames[0, 2, :, :7] = 255  # saturated border columns
     frames[1, 1, -3:, :] = 0
@@ -272,9 +274,10 @@ def test_u8_finest_level_matches_f64_frames_bitwise(device, w, h):
         a, sa = device.solve_batch(frames, EnergyParams(), S)
         b, sb = device.solve_batch(f64, EnergyParams(), S)
         for x, y, u, v in zip(a, b, sa, sb):
-            assert np.array_equal(x.grid_total, y.grid_total)
+            assert np.abs(x.grid_total - y.grid_total).max() < 1e-9
             assert np.array_equal(x.vis4, y.vis4)
-            assert u.energy_after == v.energy_after
+            for eu, ev in zip(u.energy_after, v.energy_after):
+                np.testing.assert_allclose(eu, ev, rtol=1e-12)
 
 
 def test_cfg2_full_size_properties(device):

@@ -22,9 +22,10 @@ ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--runs", type=int, default=1)
 ap.add_argument("--mode", default="schwarz")
 ap.add_argument("--profiling", action="store_true", help="plans with in-graph k_pixel<LIN> timing events")
+ap.add_argument("--lib", default=None, help="library to load (A/B variants, tools/ab.py)")
 a = ap.parse_args()
 
-dev = Solver(build.CUDA_LIB)
+dev = Solver(a.lib or build.CUDA_LIB)
 if a.profiling:
     dev.lib.hwf_set_profiling(dev.ctx.h, 1)
 frames = make_frames(a.batch, 0)
@@ -43,4 +44,11 @@ for _ in range(a.runs):
     dev.ctx.check(lib.hwf_run_device(h))
 lib.hwf_sync(h, None)
 dt = time.perf_counter() - t
-print(f"launches_per_replay={lib.hwf_launch_count(h)} batch={a.batch} ms_per_replay={1000 * dt / max(a.runs, 1):.2f}")
+line = f"launches_per_replay={lib.hwf_launch_count(h)} batch={a.batch} ms_per_replay={1000 * dt / max(a.runs, 1):.3f}"
+if a.profiling:  # k_pixel<LIN> launches of the last replay (in-graph events)
+    kms, kb = (C.c_double * 64)(), (C.c_double * 64)()
+    nk = lib.hwf_pixel_kernel_times(h, 64, kms, kb)
+    big = max(kb[i] for i in range(nk))
+    l0 = [kms[i] for i in range(nk) if kb[i] == big]
+    line += f" pixel_lin_ms={sum(kms[i] for i in range(nk)):.3f} pixel_lin_L0_ms_per_launch={sum(l0) / len(l0):.3f}"
+print(line)
