@@ -234,6 +234,60 @@ def cpu_baseline(steps: int, warmup: int, mode: str, threads: int | None = None)
                       f"threads={cores}, after {warmup} warm-up pairs", "seconds": dt}
 
 
+def e2e_flowresult(dev, lib, h, frames_np, pc, sc, steps, ws, ok, batch: int = 64) -> dict:
+    """The reference's full output contract end to end: every pair returns the dense FlowResult
+    (geometry.hpp:26-37: s, m, d and disparity per pixel as f64, vis4) plus the finest grid, through the streaming
+    public API from/to pinned host memory (two batches in flight, each slot with its own device buffers). This is
+    what the CPU reference arm produces per pair (hwflow.py run_scene_flow), so it is the like-for-like e2e
+    number. `batch` pairs per step (64: 1.1 GB of results per step, pinned twice); it is PCIe-bound."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1610_07159_b200 import capi
+    from paper_1610_07159_b200.capi import DTYPE_U8, Frame4C, ResultC, StatsC
+    from paper_1610_07159_b200.hwflow import grid_dims
+    Bd = min(batch, frames_np.shape[0])
+    N = W_ * H_
+    gw, gh = grid_dims(W_, H_, 8)
+    G = gw * gh
+    host_in = torch.from_numpy(np.ascontiguousarray(frames_np[:Bd])).pin_memory()
+    per = {"s": 2 * N, "m": 2 * N, "d": 2 * N, "disparity": N, "grid_total": 6 * G}
+    slots = [{k: torch.empty((Bd, v), dtype=torch.float64).pin_memory() for k, v in per.items()} for _ in range(2)]
+    vis = [torch.empty((Bd, N), dtype=torch.uint8).pin_memory() for _ in range(2)]
+    fr = (Frame4C * Bd)()
+    res = [(ResultC * Bd)() for _ in range(2)]
+    for i in range(Bd):
+        fr[i].width, fr[i].height, fr[i].dtype = W_, H_, DTYPE_U8
+        for e in range(4):
+            fr[i].plane[e] = host_in.data_ptr() + (4 * i + e) * N
+        for k in range(2):
+            for name, t in slots[k].items():
+                setattr(res[k][i], name, C.cast(t.data_ptr() + i * t.shape[1] * 8, capi._dp))
+            res[k][i].vis4 = C.cast(vis[k].data_ptr() + i * N, capi._u8p)
+    stats = [(StatsC * Bd)() for _ in range(2)]
+
+    def run(n):
+        for i in range(n):
+            ok(lib.hwf_submit_batch(h, Bd, fr, C.byref(pc), C.byref(sc), capi.dptr(None), res[i % 2], stats[i % 2]))
+            if i >= 1:
+                ok(lib.hwf_wait(h))
+        ok(lib.hwf_wait(h))
+
+    run(3)  # plan build + both slots' graphs
+    torch.cuda.synchronize()
+    barrier(ws)
+    t0 = time.perf_counter()
+    run(steps)
+    t1 = time.perf_counter()
+    barrier(ws)
+    sec = allreduce_max(t1 - t0, ws)
+    d2h = Bd * (8 * (7 * N + 6 * G) + N)
+    return {"value": ws * Bd * steps / sec, "unit": UNIT, "pairs_per_step": Bd, "h2d_bytes_per_step": Bd * 4 * N,
+            "d2h_bytes_per_step": d2h, "d2h_gbs": d2h * steps / sec / 1e9,
+            "note": "dense FlowResult (s, m, d, disparity f64 + vis4) + grid per pair, streaming API, pinned host memory"}
+
+
 def dist_init():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -386,6 +440,18 @@ def run_ours(args, ws, rank, local):
         v = prof.get("dram_bytes_per_launch_L0")
         traffic = v * B / prof.get("batch", 128) if v is not None else None
     launches = lib.hwf_launch_count(h)
+    # FP64 roofline of the same kernel: FP64 flops per launch from the committed ncu capture (scaled by the batch),
+    # over this run's CUDA-event launch time, against the builder-measured DFMA peak (profiles/fp64_peak.json)
+    fp64 = None
+    if prof.get("fp64_flop_per_launch_L0"):
+        flop = prof["fp64_flop_per_launch_L0"] * B / prof.get("batch", 128)
+        inst = sum(prof["fp64_inst_per_launch_L0"].values()) * B / prof.get("batch", 128)
+        fpk = json.loads((ROOT / "profiles" / "fp64_peak.json").read_text())
+        ach = flop / (l0_ms / 1000.0) / 1e12 if l0_ms > 0 else 0.0
+        inst_peak = fpk["dadd_inst_per_s"]  # FP64 pipe issue ceiling (64 lanes / clk / SM)
+        fp64 = {"achieved": ach, "peak": fpk["fp64_tflops"], "unit": "TFLOP/s", "frac": ach / fpk["fp64_tflops"],
+                "pipe_inst_frac": inst / (l0_ms / 1000.0) / inst_peak if l0_ms > 0 else None,
+                "flop_per_launch": flop, "peak_src": "profiles/fp64_peak.json (builder-measured DFMA, tools/fp64_peak.cu)"}
 
     # ---- e2e: through the public C-ABI from pinned host buffers ---------------------
     barrier(ws)
@@ -405,6 +471,7 @@ def run_ours(args, ws, rank, local):
                                     [synthetic.webcam_truth(i) for i in range(pairs.start, pairs.start + B)])
     gn_total = sum(S.gn_for_level(l) for l in range(4))
     lib.hwf_set_profiling(h, 0)  # the side measurements build their own plans, without timing events
+    e2e_fr = None if args.no_flowresult else e2e_flowresult(dev, lib, h, frames_np, pc, sc, args.steps, ws, ok)
     extra = extra_configs(dev, lib, h, C, capi) if (rank == 0 and ws == 1 and not args.no_extra) else None
     if rank == 0:
         cb = cpu_baseline(max(1, min(3, args.steps)), 1, args.mode) if ws == 1 and not args.no_cpu else None
@@ -426,9 +493,11 @@ def run_ours(args, ws, rank, local):
                          # not HBM-bound: the limiter and pipe utilisations of the same kernel from the committed
                          # ncu --set full capture (profiles/pixel_traffic.json)
                          "limiter": prof.get("limiter"), "fp64_pipe_frac": prof.get("fp64_pipe_frac"),
-                         "l1_lsu_frac": prof.get("l1_lsu_frac"), "issue_slots_frac": prof.get("issue_slots_frac")},
+                         "l1_lsu_frac": prof.get("l1_lsu_frac"), "issue_slots_frac": prof.get("issue_slots_frac"),
+                         "fp64": fp64},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": B * 4 * N,
                     "d2h_bytes_per_step": B * (G * 6 * 8 + N)},
+            "e2e_flowresult": e2e_fr,
             "gpu_launches": launches * args.steps,
             "clocks": clk.summary(),
             "solver_status": "diverged-flag" if (rc_sync == capi.HWF_EDIVERGED or rc_div == capi.HWF_EDIVERGED) else "ok",
@@ -492,6 +561,7 @@ def main():
     ap.add_argument("--mode", choices=["schwarz", "global"], default="global")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-extra", action="store_true", help="skip the cfg3/cfg5 side measurements")
+    ap.add_argument("--no-flowresult", action="store_true", help="skip the dense-FlowResult e2e leg")
     ap.add_argument("--dry", action="store_true", help="multi-rank plumbing only (gloo, no GPU work)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -271,13 +271,15 @@ int hwf_submit_batch(hwf_ctx* ctx, int n, const hwf_frame4* frames, const hwf_en
     if (ctx->inflight.size() >= 2) throw InvalidArg("two batches in flight: call hwf_wait first");
     check_params(params, sched, F);
     const int w = frames[0].width, h = frames[0].height, dt = frames[0].dtype;
+    unsigned om = 0;
     for (int i = 0; i < n; ++i) {
       if (frames[i].width != w || frames[i].height != h || frames[i].dtype != dt)
         throw InvalidArg("all pairs of a batch must share size and dtype");
-      if (out[i].s || out[i].m || out[i].d || out[i].disparity)
-        throw InvalidArg("streaming returns grid_total and vis4 only (dense fields: hwf_solve_batch)");
+      om |= (out[i].s ? 1u : 0u) | (out[i].m ? 2u : 0u) | (out[i].d ? 4u : 0u) | (out[i].disparity ? 8u : 0u);
     }
-    Plan& p = get_plan(ctx, n, w, h, dt, params, sched, F, 0u);
+    if (!ctx->inflight.empty() && ctx->plan && ctx->plan->outmask != om)
+      throw InvalidArg("batches in flight must request the same dense fields");
+    Plan& p = get_plan(ctx, n, w, h, dt, params, sched, F, om);
     if (!ctx->h2d) {
       CK(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
       CK(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
@@ -304,6 +306,7 @@ int hwf_submit_batch(hwf_ctx* ctx, int n, const hwf_frame4* frames, const hwf_en
     CK(cudaEventRecord(p.ev_h2d[k], ctx->h2d));
     // compute, then snapshot the results the next graph would overwrite
     CK(cudaStreamWaitEvent(ctx->stream, p.ev_h2d[k], 0));
+    if (om) CK(cudaStreamWaitEvent(ctx->stream, p.ev_d2h[k], 0));  // slot k's dense fields are downloaded
     CK(cudaGraphLaunch(p.exec_slot[k], ctx->stream));
     CK(cudaMemcpyAsync(p.st_grid[k], p.lv[0].total, sizeof(double) * n * G * 6, cudaMemcpyDeviceToDevice, ctx->stream));
     CK(cudaMemcpyAsync(p.st_occ[k], p.lv[0].occ, n * N, cudaMemcpyDeviceToDevice, ctx->stream));
@@ -318,6 +321,13 @@ int hwf_submit_batch(hwf_ctx* ctx, int n, const hwf_frame4* frames, const hwf_en
         CK(cudaMemcpyAsync(out[i].grid_total, p.st_grid[k] + i * G * 6, G * 6 * sizeof(double), cudaMemcpyDeviceToHost,
                            ctx->d2h));
       if (out[i].vis4) CK(cudaMemcpyAsync(out[i].vis4, p.st_occ[k] + i * N, N, cudaMemcpyDeviceToHost, ctx->d2h));
+      // dense FlowResult fields (geometry.hpp:26-37) straight from slot k's own buffers
+      double* const* o = p.o_slot[k];
+      if (out[i].s) CK(cudaMemcpyAsync(out[i].s, o[0] + i * N * 2, N * 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->d2h));
+      if (out[i].m) CK(cudaMemcpyAsync(out[i].m, o[1] + i * N * 2, N * 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->d2h));
+      if (out[i].d) CK(cudaMemcpyAsync(out[i].d, o[2] + i * N * 2, N * 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->d2h));
+      if (out[i].disparity)
+        CK(cudaMemcpyAsync(out[i].disparity, o[3] + i * N, N * sizeof(double), cudaMemcpyDeviceToHost, ctx->d2h));
     }
     CK(cudaMemcpyAsync(p.h_red[k], p.st_red[k], sizeof(double) * n * p.E.nslots * kNumEnergy, cudaMemcpyDeviceToHost,
                        ctx->d2h));

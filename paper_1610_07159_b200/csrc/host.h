@@ -343,6 +343,7 @@ struct Plan {
   Energies E;
   int* flags = nullptr;
   double *o_s = nullptr, *o_m = nullptr, *o_d = nullptr, *o_disp = nullptr;
+  double* o_slot[2][4] = {{nullptr, nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr, nullptr}};  // streaming
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   cudaStream_t side = nullptr;  // capture-time branch for the per-level E_after pass
@@ -404,6 +405,12 @@ struct Plan {
     const size_t N0 = lv[0].N, G0 = lv[0].G;
     in_slot[0] = in;
     in_slot[1] = alloc_input(N0);
+    // dense FlowResult fields: slot 1's graph writes its own copies, so a batch's download never races
+    // the next batch's solve (slot 0 keeps the plan's buffers)
+    double** o[4] = {&o_s, &o_m, &o_d, &o_disp};
+    for (int f = 0; f < 4; ++f) o_slot[0][f] = *o[f];
+    for (int f = 0; f < 4; ++f)
+      o_slot[1][f] = (outmask >> f & 1) ? mem.alloc<double>(B * N0 * (f == 3 ? 1 : 2)) : nullptr;
     for (int k = 0; k < 2; ++k) {
       st_grid[k] = mem.alloc<double>(B * G0 * 6);
       st_occ[k] = mem.alloc<uint8_t>(B * N0);
@@ -417,7 +424,11 @@ struct Plan {
     }
     // capture the same pipeline reading slot 1 (w_i ping-pong restarts from buffer a)
     for (int l = 0; l < L; ++l) lv[l].nodew = lv[l].nodew_a;
-    in = in_slot[1];
+    auto use_slot = [&](int k) {
+      in = in_slot[k];
+      for (int f = 0; f < 4; ++f) *o[f] = o_slot[k][f];
+    };
+    use_slot(1);
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     try {
       record(st);
@@ -425,13 +436,13 @@ struct Plan {
       cudaGraph_t g = nullptr;
       cudaStreamEndCapture(st, &g);
       if (g) cudaGraphDestroy(g);
-      in = in_slot[0];
+      use_slot(0);
       throw;
     }
     CK(cudaStreamEndCapture(st, &graph2));
     CK(cudaGraphInstantiate(&exec_slot[1], graph2, 0));
     exec_slot[0] = exec;
-    in = in_slot[0];
+    use_slot(0);
     async_ready = true;
   }
 

@@ -399,6 +399,44 @@ def test_streaming_submit_wait_matches_sync(device):
             assert st[i].energy_after[0][1] == stats_ref[i].energy_after[0][1]
 
 
+def test_streaming_dense_flowresult_matches_sync(device):
+    """The streaming API with the reference's full FlowResult (geometry.hpp:26-37: s, m, d, disparity, vis4 per
+    pixel, plus the grid): four batches, two in flight, each slot writing its own dense buffers; every field
+    bitwise what hwf_solve_batch returns."""
+    import ctypes as C
+    from paper_1610_07159_b200 import capi
+    w, h, n = 96, 72, 3
+    frames = [np.stack([synthetic.webcam_pair(3 * k + i, w, h)[0] for i in range(n)]) for k in range(4)]
+    S = SolveSchedule(levels=3, grid_step=8, pcg_iters=5, subdomain_px=0)
+    P = EnergyParams()
+    ref = [device.solve_batch(f, P, S)[0] for f in frames]
+    lib, hh = device.lib, device.ctx.h
+    gw, gh = grid_dims(w, h, 8)
+    pc, sc = P.to_c(), S.to_c()
+    keep = []
+    for k, f in enumerate(frames):
+        fr, res, st = (capi.Frame4C * n)(), (capi.ResultC * n)(), (capi.StatsC * n)()
+        o = {"s": np.empty((n, h, w, 2)), "m": np.empty((n, h, w, 2)), "d": np.empty((n, h, w, 2)),
+             "disparity": np.empty((n, h, w)), "vis4": np.empty((n, h, w), np.uint8), "grid_total": np.empty((n, gw * gh, 6))}
+        for i in range(n):
+            fr[i].width, fr[i].height, fr[i].dtype = w, h, capi.DTYPE_U8
+            for e in range(4):
+                fr[i].plane[e] = f[i, e].ctypes.data
+            res[i].s, res[i].m, res[i].d = capi.dptr(o["s"][i]), capi.dptr(o["m"][i]), capi.dptr(o["d"][i])
+            res[i].disparity, res[i].grid_total = capi.dptr(o["disparity"][i]), capi.dptr(o["grid_total"][i])
+            res[i].vis4 = capi.u8ptr(o["vis4"][i])
+        keep.append((fr, res, st, o, f))
+        device.ctx.check(lib.hwf_submit_batch(hh, n, fr, C.byref(pc), C.byref(sc), capi.dptr(None), res, st))
+        if k >= 1:
+            device.ctx.check(lib.hwf_wait(hh))
+    device.ctx.check(lib.hwf_wait(hh))
+    for k in range(4):
+        o = keep[k][3]
+        for i in range(n):
+            for name in ("s", "m", "d", "disparity", "vis4", "grid_total"):
+                assert np.array_equal(o[name][i], getattr(ref[k][i], name)), (k, i, name)
+
+
 def test_residual_vector_matches_oracle(device, oracle, golden):
     """assemble_residuals (energy.cpp:208-228): the stacked R, M = 2N + 14G entries."""
     for P in (EnergyParams(), EnergyParams.preset("facial")):
