@@ -17,7 +17,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIBDIR = PKG / "lib"
-CUDA_LIB = LIBDIR / "libhwflow_cuda.so"
+# HWF_CUDA_LIB: run the test suite against an A/B variant build (lib/variants/<name>/libhwflow_cuda.so)
+CUDA_LIB = Path(os.environ["HWF_CUDA_LIB"]) if os.environ.get("HWF_CUDA_LIB") else LIBDIR / "libhwflow_cuda.so"
 ORACLE_DIR = ROOT / "oracle"
 ORACLE_LIB = ORACLE_DIR / "_build" / "libhwflow_oracle.so"
 REF_LIB = ORACLE_DIR / "_ref" / "libhwflow_ref.so"
@@ -50,7 +51,7 @@ def build_cuda(force: bool = False, verbose: bool = False, defines: tuple[str, .
     """The product library; with `defines` (e.g. ("HWF_PIX_MINB=3",)) an A/B variant built to
     lib/variants/<variant>/libhwflow_cuda.so (tools/ab.py)."""
     objdir = LIBDIR / "obj" if variant is None else LIBDIR / "variants" / variant / "obj"
-    out = CUDA_LIB if variant is None else LIBDIR / "variants" / variant / "libhwflow_cuda.so"
+    out = LIBDIR / "libhwflow_cuda.so" if variant is None else LIBDIR / "variants" / variant / "libhwflow_cuda.so"
     objdir.mkdir(parents=True, exist_ok=True)
     dflags = [f"-D{d}" for d in defines]
     headers = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + list((ROOT / "include").glob("*.h"))
