@@ -62,6 +62,10 @@ const char* hwf_split_swept(int s);
 
 /* Steps (enqueued on the context stream; no host synchronisation). */
 int hwf_split_begin(hwf_split* sp, const hwf_frame4* frame);  /* upload, pyramid (replicated) */
+/* hwf_split_begin in two halves, so that everything after the upload can be captured into one CUDA graph
+ * (split.py SplitGraph): the frame upload (not capturable from pageable memory), then the pyramid. */
+int hwf_split_upload(hwf_split* sp, const hwf_frame4* frame);
+int hwf_split_prologue(hwf_split* sp);
 int hwf_split_level_begin(hwf_split* sp, int level);           /* init / prolongation (replicated) */
 int hwf_split_linearize(hwf_split* sp, int level, int it);     /* own rows + overlap */
 int hwf_split_sweep(hwf_split* sp, int level, int s);          /* own subdomains (Schwarz mode) */

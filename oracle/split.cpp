@@ -66,6 +66,7 @@ struct hwf_split {
   int dims[4 * HWF_MAX_LEVELS] = {};
   int gn[HWF_MAX_LEVELS] = {}, slot_base[HWF_MAX_LEVELS] = {};
   std::vector<double> pyr;
+  std::vector<std::vector<double>> frames;  // hwf_split_upload
   std::vector<size_t> off;
   Lev lev[HWF_MAX_LEVELS];
   std::vector<double> energy;  // [slot] partial Sum r^2 over owned rows
@@ -244,11 +245,23 @@ int hwf_split_row_elems(hwf_split* sp, int level, const char* name, long long* e
 
 const char* hwf_split_swept(int s) { return (s & 1) ? "xa" : "xb"; }
 
-int hwf_split_begin(hwf_split* sp, const hwf_frame4* frame) {
+int hwf_split_upload(hwf_split* sp, const hwf_frame4* frame) {
   return guard(sp, [&] {
     if (!frame || frame->width != sp->w || frame->height != sp->h || frame->dtype != sp->dtype)
       throw std::invalid_argument("frame does not match the split");
-    const auto imgs = orc::load_frames(frame);
+    sp->frames = orc::load_frames(frame);
+  });
+}
+
+int hwf_split_begin(hwf_split* sp, const hwf_frame4* frame) {
+  const int rc = hwf_split_upload(sp, frame);  // (declared in hwflow_split.h)
+  return rc != HWF_OK ? rc : hwf_split_prologue(sp);
+}
+
+int hwf_split_prologue(hwf_split* sp) {
+  return guard(sp, [&] {
+    if (sp->frames.empty()) throw std::invalid_argument("hwf_split_prologue before hwf_split_upload");
+    const auto& imgs = sp->frames;
     sp->pyr.assign(sp->off[sp->L], 0.0);
     orc::backend()->pyramid(imgs, sp->w, sp->h, sp->L, sp->pyr.data());
     for (int l = 0; l < sp->L; ++l) {  // buffers the driver may query before level_begin

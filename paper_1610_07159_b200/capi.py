@@ -161,6 +161,8 @@ _SPLIT_SIGS = {  # include/hwflow_split.h (both the CUDA library and the oracle)
     "hwf_split_buffer": (C.c_int, [C.c_void_p, C.c_int, C.c_char_p, _vpp, C.POINTER(C.c_longlong)]),
     "hwf_split_swept": (C.c_char_p, [C.c_int]),
     "hwf_split_begin": (C.c_int, [C.c_void_p, C.POINTER(Frame4C)]),
+    "hwf_split_upload": (C.c_int, [C.c_void_p, C.POINTER(Frame4C)]),
+    "hwf_split_prologue": (C.c_int, [C.c_void_p]),
     "hwf_split_level_begin": (C.c_int, [C.c_void_p, C.c_int]),
     "hwf_split_linearize": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
     "hwf_split_sweep": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),

@@ -160,7 +160,7 @@ int hwf_split_row_elems(hwf_split* sp, int level, const char* name, long long* e
 
 const char* hwf_split_swept(int s) { return (s & 1) ? "xa" : "xb"; }
 
-int hwf_split_begin(hwf_split* sp, const hwf_frame4* frame) {
+int hwf_split_upload(hwf_split* sp, const hwf_frame4* frame) {
   return guard(sp ? sp->ctx : nullptr, [&] {
     checked(sp);
     Plan& p = *sp->plan;
@@ -169,8 +169,16 @@ int hwf_split_begin(hwf_split* sp, const hwf_frame4* frame) {
     for (int e = 0; e < 4; ++e)
       if (!frame->plane[e]) throw InvalidArg("null image plane");
     upload_frames(p, 1, frame, sp->ctx->stream);
-    p.rec_prologue(sp->ctx->stream, sp->LC);
   });
+}
+
+int hwf_split_prologue(hwf_split* sp) {
+  return guard(sp ? sp->ctx : nullptr, [&] { checked(sp)->plan->rec_prologue(sp->ctx->stream, sp->LC); });
+}
+
+int hwf_split_begin(hwf_split* sp, const hwf_frame4* frame) {
+  const int rc = hwf_split_upload(sp, frame);
+  return rc != HWF_OK ? rc : hwf_split_prologue(sp);
 }
 
 int hwf_split_level_begin(hwf_split* sp, int level) {

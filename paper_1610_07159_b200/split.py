@@ -93,6 +93,12 @@ class SplitRank:
     def begin(self, frame: Frame4C):
         self._check(self.lib.hwf_split_begin(self.h, C.byref(frame)))
 
+    def upload(self, frame: Frame4C):
+        self._check(self.lib.hwf_split_upload(self.h, C.byref(frame)))
+
+    def prologue(self):
+        self._check(self.lib.hwf_split_prologue(self.h))
+
     def level_begin(self, l: int):
         self._check(self.lib.hwf_split_level_begin(self.h, l))
 
@@ -308,14 +314,12 @@ def _pcg_split(ranks: list[SplitRank], comm, l: int):
             comm.halo(ranks, l, "z")
 
 
-def solve_split(ranks: list[SplitRank], comm, images: np.ndarray) -> list[tuple[FlowResult, GnStats]]:
-    """run_scene_flow (SPEC.md:396-404) of one frame pair (4, h, w), split across `ranks`
-    (all of them for LocalComm, this process's one for TorchComm). Returns each local rank's
-    (FlowResult, GnStats); every rank ends with the full result."""
-    frame, keep = _frame(images)
-    for r in ranks:
-        r.begin(frame)
+def _split_body(ranks: list[SplitRank], comm):
+    """Everything between the frame upload and hwf_split_finish: device enqueues and collectives only (no host
+    synchronisation), so that SplitGraph can capture it into one CUDA graph."""
     r0 = ranks[0]
+    for r in ranks:
+        r.prologue()
     for l in reversed(range(r0.levels)):
         for r in ranks:
             r.level_begin(l)
@@ -338,6 +342,54 @@ def solve_split(ranks: list[SplitRank], comm, images: np.ndarray) -> list[tuple[
             r.level_end(l)
     comm.allreduce_sum(ranks, "energy")
     comm.allreduce_or(ranks, "flags")
+
+
+def solve_split(ranks: list[SplitRank], comm, images: np.ndarray) -> list[tuple[FlowResult, GnStats]]:
+    """run_scene_flow (SPEC.md:396-404) of one frame pair (4, h, w), split across `ranks`
+    (all of them for LocalComm, this process's one for TorchComm). Returns each local rank's
+    (FlowResult, GnStats); every rank ends with the full result."""
+    frame, keep = _frame(images)
+    for r in ranks:
+        r.upload(frame)
+    _split_body(ranks, comm)
     out = [r.finish() for r in ranks]
     del keep
     return out
+
+
+class SplitGraph:
+    """The split solve as ONE CUDA graph per process: the steps of every local rank, the halo exchanges and the
+    PCG dot-partial all-gathers (NCCL collectives under TorchComm, device copies under LocalComm) are captured
+    once; a frame is then upload -> graph replay -> finish, with no host code between PCG phases.
+    Device libraries only (the CPU oracle has no graphs)."""
+
+    def __init__(self, ranks: list[SplitRank], comm, images: np.ndarray):
+        if not all(r.on_device for r in ranks):
+            raise ValueError("SplitGraph needs the CUDA library")
+        self.ranks, self.comm = ranks, comm
+        stream = ranks[0].stream
+        frame, keep = _frame(images)
+        for r in ranks:  # warm-up: plans, workspaces and NCCL communicators exist before capture
+            r.upload(frame)
+        _split_body(ranks, comm)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=stream):
+            _split_body(ranks, comm)
+        torch.cuda.synchronize()
+        del keep
+
+    def replay(self):
+        """The captured solve on the frame last uploaded (device time only; no transfers), launched on the
+        library's stream so that it is ordered after the upload and before the download."""
+        with torch.cuda.stream(self.ranks[0].stream):
+            self.graph.replay()
+
+    def __call__(self, images: np.ndarray) -> list[tuple[FlowResult, GnStats]]:
+        frame, keep = _frame(images)
+        for r in self.ranks:
+            r.upload(frame)
+        self.replay()
+        out = [r.finish() for r in self.ranks]
+        del keep
+        return out

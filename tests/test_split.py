@@ -21,7 +21,7 @@ import torch.multiprocessing as mp
 from paper_1610_07159_b200 import synthetic
 from paper_1610_07159_b200.capi import DTYPE_U8
 from paper_1610_07159_b200.hwflow import EnergyParams, SolveSchedule
-from paper_1610_07159_b200.split import LocalComm, SplitRank, solve_split
+from paper_1610_07159_b200.split import LocalComm, SplitGraph, SplitRank, solve_split
 
 SCHED = SolveSchedule(levels=3, grid_step=4, gn_per_level=[2, 2, 2], pcg_iters=4, patch_iters=3, subdomain_px=16)
 GSCHED = SolveSchedule(levels=3, grid_step=4, gn_per_level=[2, 2, 2], pcg_iters=4, subdomain_px=0)  # global PCG
@@ -154,7 +154,27 @@ def test_split_device_matches_unsplit_device(device, w, h, world, sched):
         r.close()
 
 
-def _nccl_worker(port: int, q, mode: str = "schwarz"):
+@pytest.mark.gpu
+@pytest.mark.parametrize("w,h,world,sched", [
+    (128, 96, 2, GSCHED),
+    (640, 480, 3, SolveSchedule(levels=4, grid_step=8, pcg_iters=5, subdomain_px=0)),
+    (640, 480, 2, SolveSchedule(levels=4, grid_step=8, pcg_iters=5, patch_iters=5, subdomain_px=16)),
+])
+def test_split_graph_matches_unsplit_device(device, w, h, world, sched):
+    """SplitGraph: every rank's steps and the exchanges captured into one CUDA graph (no host code between PCG
+    phases); two different frames replayed through the same graph, each bitwise the unsplit solve."""
+    ranks = [SplitRank(device, w, h, DTYPE_U8, EnergyParams(), sched, None, r, world) for r in range(world)]
+    g = SplitGraph(ranks, LocalComm(), _frames(w, h, seed=3))
+    for seed in (3, 4):
+        imgs = _frames(w, h, seed=seed)
+        ref = _unsplit(device, imgs, sched)
+        for out in g(imgs):
+            _assert_same(out, ref, 1e-12)
+    for r in ranks:
+        r.close()
+
+
+def _nccl_worker(port: int, q, mode: str = "schwarz", graph: bool = False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch
     import torch.distributed as dist
@@ -166,19 +186,22 @@ def _nccl_worker(port: int, q, mode: str = "schwarz"):
         from paper_1610_07159_b200.split import TorchComm
         solver = Solver(build.CUDA_LIB)
         me = SplitRank(solver, 128, 96, DTYPE_U8, EnergyParams(), MODES[mode], None, 0, 1)
-        ((r, st),) = solve_split([me], TorchComm(me), _frames())
+        if graph:  # the NCCL collectives captured in the CUDA graph with the library's kernels
+            ((r, st),) = SplitGraph([me], TorchComm(me), _frames())(_frames())
+        else:
+            ((r, st),) = solve_split([me], TorchComm(me), _frames())
         q.put((r.grid_total, r.vis4))
     finally:
         dist.destroy_process_group()
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode", ["schwarz", "global"])
-def test_split_nccl_single_rank(device, mode):
+@pytest.mark.parametrize("mode,graph", [("schwarz", False), ("global", False), ("global", True)])
+def test_split_nccl_single_rank(device, mode, graph):
     ref = _unsplit(device, _frames(), MODES[mode])
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    p = ctx.Process(target=_nccl_worker, args=(_free_port(), q, mode))
+    p = ctx.Process(target=_nccl_worker, args=(_free_port(), q, mode, graph))
     p.start()
     grid, vis = q.get(timeout=300)
     p.join(timeout=60)

@@ -24,10 +24,11 @@ import torch  # noqa: E402
 from paper_1610_07159_b200 import build, synthetic  # noqa: E402
 from paper_1610_07159_b200.capi import DTYPE_U8  # noqa: E402
 from paper_1610_07159_b200.hwflow import EnergyParams, SolveSchedule, Solver  # noqa: E402
-from paper_1610_07159_b200.split import LocalComm, SplitRank, solve_split  # noqa: E402
+from paper_1610_07159_b200.split import LocalComm, SplitGraph, SplitRank, solve_split  # noqa: E402
 
 NVLINK_GBS = 700.0      # assumed effective NVLink 5 P2P / all-gather rate per GPU (B200 spec: 900 GB/s/dir)
-LATENCY_US = 15.0       # assumed per-collective latency
+LATENCY_US = 15.0       # assumed per-collective latency, host-launched collectives
+GRAPH_LATENCY_US = 6.0  # assumed per-collective latency of small NCCL all-gathers inside one CUDA graph
 
 
 class Timed(SplitRank):
@@ -42,9 +43,12 @@ class Timed(SplitRank):
         e1.record(self.stream)
         self._ev.append((e0, e1))
 
-    def begin(self, f):
+    def upload(self, f):  # transfers are not busy time; the step timing starts with the pyramid
         self._ev = []
-        self._t(super().begin, f)
+        super().upload(f)
+
+    def prologue(self):
+        self._t(super().prologue)
 
     def level_begin(self, l):
         self._t(super().level_begin, l)
@@ -73,6 +77,43 @@ class Timed(SplitRank):
         return super().finish()
 
 
+class NullComm(LocalComm):
+    """No exchanges: one rank's own device work, for its busy time."""
+
+    def halo(self, *a):
+        pass
+
+    def allgather_rows(self, *a):
+        pass
+
+    def allreduce_sum(self, *a):
+        pass
+
+    def allreduce_or(self, *a):
+        pass
+
+
+def graph_busy_ms(dev, w, h, S, imgs, world: int, reps: int) -> list[float]:
+    """Per-rank device time of the rank's whole frame as one captured CUDA graph (split.py SplitGraph with the
+    exchanges left out), median of `reps` replays: no host launch gaps."""
+    out = []
+    for r in range(world):
+        rank = SplitRank(dev, w, h, DTYPE_U8, EnergyParams(), S, None, r, world)
+        g = SplitGraph([rank], NullComm(), imgs)
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(rank.stream)
+            g.replay()
+            e1.record(rank.stream)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        out.append(sorted(ts)[len(ts) // 2])
+        del g
+        rank.close()
+    return out
+
+
 class CountingComm(LocalComm):
     def __init__(self):
         self.halo_bytes = self.gather_bytes = 0
@@ -97,6 +138,7 @@ def main():
     ap.add_argument("--worlds", type=int, nargs="+", default=[1, 2, 4, 8])
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--mode", choices=["global", "schwarz"], default="global")
+    ap.add_argument("--graph", action="store_true", help="per-rank busy time from a captured CUDA graph (SplitGraph)")
     a = ap.parse_args()
     dev = Solver(build.CUDA_LIB)
     imgs = synthetic.uhd_pair(0)[0]
@@ -109,10 +151,12 @@ def main():
             comm = CountingComm()
             solve_split(ranks, comm, imgs)
         busy = [r.ms for r in ranks]
+        if a.graph:
+            busy = graph_busy_ms(dev, w, h, S, imgs, world, max(a.reps, 5))
         xfer_ms = (comm.halo_bytes + comm.gather_bytes) / (NVLINK_GBS * 1e9) * 1e3
-        lat_ms = (comm.halos + comm.gathers) * LATENCY_US / 1e3 if world > 1 else 0.0
+        lat_ms = (comm.halos + comm.gathers) * (GRAPH_LATENCY_US if a.graph else LATENCY_US) / 1e3 if world > 1 else 0.0
         proj = max(busy) + (xfer_ms + lat_ms if world > 1 else 0.0)
-        row = {"mode": a.mode, "world": world, "rank_busy_ms": [round(b, 3) for b in busy], "max_busy_ms": round(max(busy), 3),
+        row = {"mode": a.mode, "graph": a.graph, "world": world, "rank_busy_ms": [round(b, 3) for b in busy], "max_busy_ms": round(max(busy), 3),
                "exchanges": comm.halos + comm.gathers, "exchange_MB": round((comm.halo_bytes + comm.gather_bytes) / 1e6, 2),
                "projected_frame_ms": round(proj, 3), "projected_hz": round(1000.0 / proj, 1)}
         out.append(row)
