@@ -7,6 +7,7 @@
 //   hwflow::b200::gauss_newton(...)   replaces hwflow::gauss_newton   (solver.hpp:152-154)
 //   hwflow::b200::run_scene_flow(...) is run_scene_flow
 //   hwflow::b200::build_pyramid(...)  replaces hwflow::build_pyramid  (image.hpp:83)
+//   hwflow::b200::assemble_jacobian(...) replaces hwflow::assemble_jacobian (solver.hpp:106-111)
 //   hwflow::b200::{validate, triangulate_dlt, compute_scene_points, export_mesh_obj}
 //                                      are the geometry.hpp:20-59 declarations
 // Same argument meaning; SolverDivergence / std::invalid_argument are thrown
@@ -128,6 +129,47 @@ inline GnStats gauss_newton(const Device& dev, EnergyContext& ctx, const WarpGri
   st.energy_before = eb;
   st.energy_after = ea;
   return st;
+}
+
+// assemble_jacobian (solver.hpp:106-111): the derivative checker's rows, evaluated on the device.
+inline JacobianRows assemble_jacobian(const Device& dev, const EnergyContext& ctx, uint8_t active_fields = 0b111,
+                                      int negate_field = -1) {
+  hwf_level lv{};
+  lv.width = ctx.width;
+  lv.height = ctx.height;
+  lv.grid_step = ctx.total->step();
+  for (int e = 0; e < 4; ++e) {
+    lv.images[e] = ctx.images[e]->data().data();
+    lv.illum[e] = ctx.illum[e] ? ctx.illum[e]->data().data() : nullptr;
+  }
+  const std::vector<double> t = grid_to_c(*ctx.total), d = grid_to_c(*ctx.delta);
+  lv.total = t.data();
+  lv.delta = d.data();
+  lv.vis4 = ctx.weights->vis4.data();
+  lv.outlier = ctx.weights->outlier.data();
+  lv.node_w = ctx.weights->node_w.data();
+  double F[9];
+  if (ctx.fundamental) {
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) F[3 * i + j] = (*ctx.fundamental)(i, j);
+    lv.fundamental = F;
+  }
+  const hwf_energy_params p = to_c(ctx.params);
+  long long nnz = 0;
+  check(dev.get(), hwf_assemble_jacobian(dev.get(), &lv, &p, active_fields, negate_field, nullptr, nullptr, nullptr,
+                                         nullptr, 0, &nnz));
+  JacobianRows out;
+  out.rows = ctx.residual_count();
+  out.cols = 6 * ctx.node_count();
+  std::vector<double> R(out.rows), v(nnz);
+  std::vector<int> r(nnz), c(nnz);
+  check(dev.get(), hwf_assemble_jacobian(dev.get(), &lv, &p, active_fields, negate_field, R.data(), r.data(), c.data(),
+                                         v.data(), nnz, &nnz));
+  out.residuals.resize(out.rows);
+  for (int i = 0; i < out.rows; ++i) out.residuals(i) = R[i];
+  out.entries.resize(nnz);
+  for (long long i = 0; i < nnz; ++i) out.entries[i] = {r[i], c[i], v[i]};
+  return out;
 }
 
 // build_pyramid for the four inputs at once (image.cpp:177-185, bit-exact).

@@ -17,6 +17,8 @@
  *   hwf_eval_energy    -> energy_breakdown / assemble_residuals  src/energy.cpp:208-251
  *   hwf_refresh_weights-> refresh_outlier_bits / refresh_feature_weights  src/energy.cpp:253-293
  *   hwf_linearize      -> build_normal_system     src/solver.cpp:100-245
+ *   hwf_assemble_jacobian -> assemble_jacobian    src/solver.cpp:247-314 (derivative-checker hook)
+ *   hwf_normal_dense   -> NormalSystem::dense     src/solver.cpp:89-98
  *   hwf_pcg            -> pcg_solve               src/solver.cpp:365-380
  *   hwf_schwarz        -> schwarz_iterate         src/solver.cpp:414-482 (+ build_subdomains :382-412)
  *   hwf_occlusion      -> compute_occlusion_maps  SPEC.md:414-422 (no code shipped)
@@ -196,6 +198,17 @@ int hwf_refresh_weights(hwf_ctx* ctx, const hwf_level* lv, const hwf_energy_para
 int hwf_linearize(hwf_ctx* ctx, const hwf_level* lv, const hwf_energy_params* params,
                   uint32_t active_fields, double lm_lambda, double* blocks, double* rhs,
                   double* precond /*nullable*/);
+/* assemble_jacobian (include/hwflow/solver.hpp:106-111, src/solver.cpp:247-314), the reference's derivative-checker
+ * hook: the stacked residual vector R (M = 2N + 14G, residuals) and the sparse Jacobian dR/dx over the 6G unknowns
+ * as (row, col, value) triplets in the reference's order. negate_field >= 0 flips that flow field's analytic
+ * derivatives, residuals untouched (the negative control). Triplet buffers may be NULL with cap = 0 to query
+ * *nnz; HWF_EINVAL if cap < *nnz. */
+int hwf_assemble_jacobian(hwf_ctx* ctx, const hwf_level* lv, const hwf_energy_params* params,
+                          uint32_t active_fields, int negate_field, double* residuals /*M, nullable*/,
+                          int* rows, int* cols, double* vals, long long cap, long long* nnz);
+/* NormalSystem::dense (include/hwflow/solver.hpp:77, src/solver.cpp:89-98): the (6G x 6G) row-major matrix of a
+ * system given in hwf_linearize layout (for SPD / eigenvalue checks on small instances). Host-only. */
+int hwf_normal_dense(int gw, int gh, const double* blocks, double* dense);
 /* Global PCG from x0 = 0 on a system given in hwf_linearize layout.
  * trace (nullable) receives iters+1 residual norms. */
 int hwf_pcg(hwf_ctx* ctx, int grid_w, int grid_h, const double* blocks, const double* rhs,

@@ -15,6 +15,11 @@
 
 namespace orc {
 
+struct JacEntry {  // solver.hpp:96-99
+  int row, col;
+  double value;
+};
+
 struct Backend {
   virtual ~Backend() = default;
   virtual const char* name() const = 0;
@@ -28,6 +33,9 @@ struct Backend {
   virtual void linearize(const hwf_level* lv, const hwf_energy_params* P, uint32_t active,
                          double lm, double* blocks, double* rhs, double* precond,
                          int threads) = 0;
+  // assemble_jacobian (solver.cpp:247-314): residuals (M) and triplets in the reference's order
+  virtual void jacobian(const hwf_level* lv, const hwf_energy_params* P, uint32_t active, int negate_field,
+                        std::vector<double>& R, std::vector<JacEntry>& entries, int threads) = 0;
   virtual void pcg(int gw, int gh, const double* blocks, const double* rhs, int iters,
                    double* x, double* trace) = 0;
   virtual void schwarz(int gw, int gh, int step, int tile, int boundary, const double* blocks,

@@ -14,6 +14,7 @@
 //      (the test compares it with the oracle's Algorithm 1)
 //   4. SolverDivergence (core.hpp:19)       thrown by both sides on the same degenerate level
 //   5. std::invalid_argument                thrown by both sides for a negative weight (energy.cpp:43-50)
+//   6. assemble_jacobian (solver.cpp:247-314) hwflow:: vs hwflow::b200::, with the negate_field hook: same triplets
 #include <cmath>
 #include <cstdio>
 #include <fstream>
@@ -109,6 +110,27 @@ int main(int argc, char** argv) {
     for (size_t j = 0; j < trace_ref[i].size() && j < trace_dev[i].size(); ++j)
       trmax = std::max(trmax, std::abs(trace_ref[i][j] - trace_dev[i][j]) / std::max(1e-300, trace_ref[i][0]));
 
+  // 2b. assemble_jacobian (solver.cpp:247-314) on the reference's EnergyContext at the state GN left behind
+  WarpGrid tot = base.plus(delta_ref);
+  cr.total = &tot;
+  cr.delta = &delta_ref;
+  cr.weights = &wr;
+  const JacobianRows jr = assemble_jacobian(cr, 0b111, 1), jd = b200::assemble_jacobian(dev, cr, 0b111, 1);
+  bool jac_same_entries = jr.entries.size() == jd.entries.size() && jr.rows == jd.rows && jr.cols == jd.cols;
+  // max |difference| over max |value|, for the Jacobian values and the residuals separately
+  double jdiff = 0.0, jmax = 0.0, rdiff = 0.0, rmax = 0.0;
+  for (size_t i = 0; jac_same_entries && i < jr.entries.size(); ++i) {
+    jac_same_entries = jr.entries[i].row == jd.entries[i].row && jr.entries[i].col == jd.entries[i].col;
+    jdiff = std::max(jdiff, std::abs(jr.entries[i].value - jd.entries[i].value));
+    jmax = std::max(jmax, std::abs(jr.entries[i].value));
+  }
+  for (int i = 0; jac_same_entries && i < jr.rows; ++i) {
+    rdiff = std::max(rdiff, std::abs(jr.residuals(i) - jd.residuals(i)));
+    rmax = std::max(rmax, std::abs(jr.residuals(i)));
+  }
+  const double jac_rel = std::max(jdiff / std::max(jmax, 1e-300), rdiff / std::max(rmax, 1e-300));
+  cr.total = nullptr;
+
   // 3. Algorithm 1 on the device through the bridge; images (4 x f64 planes), then the FlowResult (s, m, d,
   //    disparity as f64, vis4 u8) to argv[1]
   SolveSchedule full;
@@ -166,8 +188,10 @@ int main(int argc, char** argv) {
   std::printf(
       "{\"pyramid_bit_exact\": %s, \"gn_delta_max\": %.3e, \"gn_energy_rel\": %.3e, \"gn_node_w_rel\": %.3e, "
       "\"gn_W_exact\": %s, \"pcg_trace_shape\": %s, \"pcg_trace_rel\": %.3e, \"solve_width\": %d, \"solve_height\": %d, "
-      "\"finest_gn_iters\": %zu, \"divergence_ref\": %d, \"divergence_dev\": %d, \"invalid_ref\": %d, \"invalid_dev\": %d}\n",
+      "\"finest_gn_iters\": %zu, \"divergence_ref\": %d, \"divergence_dev\": %d, \"invalid_ref\": %d, \"invalid_dev\": %d, "
+      "\"jacobian_same_entries\": %s, \"jacobian_rel\": %.3e, \"jacobian_nnz\": %zu}\n",
       pyr_exact ? "true" : "false", dmax, emax, nwmax, w_exact ? "true" : "false", trace_shape ? "true" : "false", trmax,
-      fr.width, fr.height, finest.energy_after.size(), div_ref, div_dev, inv_ref, inv_dev);
+      fr.width, fr.height, finest.energy_after.size(), div_ref, div_dev, inv_ref, inv_dev,
+      jac_same_entries ? "true" : "false", jac_rel, jr.entries.size());
   return 0;
 }

@@ -556,6 +556,72 @@ inline void mask6(double* v, uint32_t active) {  // solver.cpp:27-31
 }
 }  // namespace
 
+// solver.cpp:247-314 (assemble_jacobian): residual rows photo [0, N), grad [N, 2N), smooth [2N, 2N+6G),
+// epi [2N+6G, 2N+8G), mag [2N+8G, 2N+14G); entries in the reference's loop order.
+void assemble_jacobian(const Level& L, uint32_t active, int negate_field, std::vector<double>& R,
+                       std::vector<JacTriplet>& out) {
+  const int N = L.N(), G = L.G();
+  R.assign(static_cast<size_t>(2) * N + 14 * static_cast<size_t>(G), 0.0);
+  out.clear();
+  auto hooks = [&](double* v) {
+    mask6(v, active);
+    if (negate_field >= 0) {
+      v[2 * negate_field] *= -1.0;
+      v[2 * negate_field + 1] *= -1.0;
+    }
+  };
+  for (int pix = 0; pix < N; ++pix) {
+    const int px = pix % L.w, py = pix / L.w;
+    const PixelEval ev = eval_pixel(L, px, py, true);
+    R[pix] = ev.r_photo;
+    R[N + pix] = ev.r_grad;
+    const Support sp = support(L.g, px, py);
+    double jp[6], jg[6];
+    std::copy(ev.jp, ev.jp + 6, jp);
+    std::copy(ev.jg, ev.jg + 6, jg);
+    hooks(jp);
+    hooks(jg);
+    for (int i = 0; i < 4; ++i) {
+      if (sp.wt[i] == 0.0) continue;
+      for (int j = 0; j < 6; ++j) {
+        const int col = 6 * sp.node[i] + j;
+        if (jp[j] != 0.0) out.push_back({pix, col, sp.wt[i] * jp[j]});
+        if (jg[j] != 0.0) out.push_back({N + pix, col, sp.wt[i] * jg[j]});
+      }
+    }
+  }
+  for (int n = 0; n < G; ++n) {
+    const NodeEval ev = eval_node(L, n, true);
+    for (int row = 0; row < 6; ++row) {
+      const int r = 2 * N + 6 * n + row;
+      R[r] = ev.smooth_r[row];
+      const int f = row / 2;
+      if (!((active >> f) & 1)) continue;
+      const double sgn = f == negate_field ? -1.0 : 1.0;
+      if (ev.jc[row] != 0.0) out.push_back({r, 6 * n + row, sgn * ev.jc[row]});
+      if (ev.right >= 0 && ev.jr[row] != 0.0) out.push_back({r, 6 * ev.right + row, sgn * ev.jr[row]});
+      if (ev.down >= 0 && ev.jd[row] != 0.0) out.push_back({r, 6 * ev.down + row, sgn * ev.jd[row]});
+    }
+    for (int t = 0; t < 2; ++t) {
+      const int r = 2 * N + 6 * G + 2 * n + t;
+      R[r] = ev.epi_r[t];
+      double j[6];
+      std::copy(ev.epi_j[t], ev.epi_j[t] + 6, j);
+      hooks(j);
+      for (int c = 0; c < 6; ++c)
+        if (j[c] != 0.0) out.push_back({r, 6 * n + c, j[c]});
+    }
+    for (int row = 0; row < 6; ++row) {
+      const int r = 2 * N + 8 * G + 6 * n + row;
+      R[r] = ev.mag_r[row];
+      const int f = row / 2;
+      if (!((active >> f) & 1)) continue;
+      const double sgn = f == negate_field ? -1.0 : 1.0;
+      if (ev.mag_j[row] != 0.0) out.push_back({r, 6 * n + row, sgn * ev.mag_j[row]});
+    }
+  }
+}
+
 // solver.cpp:100-245
 System build_normal_system(const Level& L, uint32_t active, double lm_lambda) {
   const int gw = L.g.gw, gh = L.g.gh, step = L.g.step, N = L.N(), G = L.G();

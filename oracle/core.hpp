@@ -125,6 +125,12 @@ struct System {  // solver.hpp:41-87
 inline int slot(int dx, int dy) { return (dy + 1) * 3 + (dx + 1); }
 
 System build_normal_system(const Level& L, uint32_t active, double lm_lambda);
+struct JacTriplet {
+  int row, col;
+  double value;
+};
+void assemble_jacobian(const Level& L, uint32_t active, int negate_field, std::vector<double>& R,
+                       std::vector<JacTriplet>& out);  // solver.cpp:247-314
 std::vector<double> pcg_solve(const System& S, int iters, std::vector<double>* trace);
 struct Subdomain {
   std::vector<int> interior;

@@ -548,6 +548,44 @@ int hwf_linearize(hwf_ctx* ctx, const hwf_level* lv, const hwf_energy_params* p,
     orc::backend()->linearize(lv, p, active, lm, blocks, rhs, precond, ctx ? ctx->threads : 1);
   });
 }
+int hwf_assemble_jacobian(hwf_ctx* ctx, const hwf_level* lv, const hwf_energy_params* p, uint32_t active,
+                          int negate_field, double* residuals, int* rows, int* cols, double* vals, long long cap,
+                          long long* nnz) {
+  return orc::guard(ctx, [&] {
+    if (!lv || !p || !nnz || negate_field < -1 || negate_field > 2) throw std::invalid_argument("bad jacobian query");
+    std::vector<double> R;
+    std::vector<orc::JacEntry> e;
+    orc::backend()->jacobian(lv, p, active, negate_field, R, e, 1);
+    *nnz = static_cast<long long>(e.size());
+    if (residuals) std::memcpy(residuals, R.data(), R.size() * sizeof(double));
+    if (cap > 0 || rows || cols || vals) {
+      if (cap < *nnz || !rows || !cols || !vals) throw std::invalid_argument("jacobian triplet buffers too small");
+      for (size_t i = 0; i < e.size(); ++i) {
+        rows[i] = e[i].row;
+        cols[i] = e[i].col;
+        vals[i] = e[i].value;
+      }
+    }
+  });
+}
+
+int hwf_normal_dense(int gw, int gh, const double* blocks, double* dense) {  // solver.cpp:89-98
+  if (gw < 1 || gh < 1 || !blocks || !dense) return HWF_EINVAL;
+  const long long G = static_cast<long long>(gw) * gh, D = 6 * G;
+  std::fill(dense, dense + D * D, 0.0);
+  for (long long n = 0; n < G; ++n)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        const long long a = n % gw + dx, b = n / gw + dy;
+        if (a < 0 || a >= gw || b < 0 || b >= gh) continue;
+        const long long nb = b * gw + a;
+        const double* B = blocks + (n * 9 + (dy + 1) * 3 + (dx + 1)) * 36;
+        for (int i = 0; i < 6; ++i)
+          for (int j = 0; j < 6; ++j) dense[(6 * n + i) * D + 6 * nb + j] = B[6 * i + j];
+      }
+  return HWF_OK;
+}
+
 int hwf_pcg(hwf_ctx* ctx, int gw, int gh, const double* blocks, const double* rhs, int iters,
             double* x, double* trace) {
   return orc::guard(ctx, [&] { orc::backend()->pcg(gw, gh, blocks, rhs, iters, x, trace); });

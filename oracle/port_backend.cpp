@@ -63,6 +63,13 @@ struct Port final : Backend {
                  double* blocks, double* rhs, double* precond, int threads) override {
     copy_system(build_normal_system(make_level(lv, P, threads), active, lm), blocks, rhs, precond);
   }
+  void jacobian(const hwf_level* lv, const hwf_energy_params* P, uint32_t active, int negate_field,
+                std::vector<double>& R, std::vector<JacEntry>& entries, int threads) override {
+    std::vector<JacTriplet> t;
+    assemble_jacobian(make_level(lv, P, threads), active, negate_field, R, t);
+    entries.resize(t.size());
+    for (size_t i = 0; i < t.size(); ++i) entries[i] = {t[i].row, t[i].col, t[i].value};
+  }
   void pcg(int gw, int gh, const double* blocks, const double* rhs, int iters, double* x,
            double* trace) override {
     const System S = load_system(gw, gh, blocks, rhs);

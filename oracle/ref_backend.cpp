@@ -156,6 +156,19 @@ struct Ref final : Backend {
     std::memcpy(outlier, L.wts.outlier.data(), L.wts.outlier.size());
     std::memcpy(node_w, L.wts.node_w.data(), L.wts.node_w.size() * sizeof(double));
   }
+  void jacobian(const hwf_level* lv, const hwf_energy_params* P, uint32_t active, int negate_field,
+                std::vector<double>& R, std::vector<JacEntry>& entries, int threads) override {
+    guard([&] {
+      RefLevel L(lv, P, threads);
+      const hwflow::JacobianRows J = hwflow::assemble_jacobian(L.ctx, static_cast<uint8_t>(active), negate_field);
+      R.resize(J.rows);
+      for (int i = 0; i < J.rows; ++i) R[i] = J.residuals(i);
+      entries.resize(J.entries.size());
+      for (size_t i = 0; i < J.entries.size(); ++i)
+        entries[i] = {J.entries[i].row, J.entries[i].col, J.entries[i].value};
+      return 0;
+    });
+  }
   void linearize(const hwf_level* lv, const hwf_energy_params* P, uint32_t active, double lm,
                  double* blocks, double* rhs, double* precond, int threads) override {
     guard([&] {

@@ -119,6 +119,10 @@ _SIGS = {
     "hwf_refresh_weights": (C.c_int, [C.c_void_p, C.POINTER(LevelC), C.POINTER(EnergyParamsC), _u8p, _dp]),
     "hwf_linearize": (C.c_int, [C.c_void_p, C.POINTER(LevelC), C.POINTER(EnergyParamsC), C.c_uint32, C.c_double,
                                 _dp, _dp, _dp]),
+    "hwf_assemble_jacobian": (C.c_int, [C.c_void_p, C.POINTER(LevelC), C.POINTER(EnergyParamsC), C.c_uint32, C.c_int,
+                                        _dp, C.POINTER(C.c_int), C.POINTER(C.c_int), _dp, C.c_longlong,
+                                        C.POINTER(C.c_longlong)]),
+    "hwf_normal_dense": (C.c_int, [C.c_int, C.c_int, _dp, _dp]),
     "hwf_pcg": (C.c_int, [C.c_void_p, C.c_int, C.c_int, _dp, _dp, C.c_int, _dp, _dp]),
     "hwf_schwarz": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp, C.c_int, C.c_int,
                               _dp]),

@@ -42,6 +42,7 @@ struct PixArgs {
   // strip split (hwflow_split.h): pixel-tile rows [ty0, ty1) are computed, rows [own0, own1)
   // contribute energy partials (others write zeros); ty1 <= 0 = the whole level
   int ty0, ty1, own0, own1;
+  double* jac;          // test hook (hwf_assemble_jacobian, LIN): per pixel {r_p, r_g, J_p[6], J_g[6]}, or null
 };
 
 struct NodeArgs {
@@ -69,7 +70,9 @@ struct NodeArgs {
   // strip split: nodes [n_lo, n_hi) are assembled, nodes [own_lo, own_hi) contribute energy
   // partials; n_hi <= 0 = the whole level
   int n_lo, n_hi, own_lo, own_hi;
+  double* jac;  // test hook (hwf_assemble_jacobian, LIN): per node kNodeJac doubles (eval_node rows), or null
 };
+constexpr int kNodeJac = 50;  // smooth r, jc, jr, jd (4 x 6), epi r (2), epi j (2 x 6), mag r (6), mag j (6)
 
 struct SwzArgs {
   int gw, gh, step, tile, ntx, nty, nxm, nym;

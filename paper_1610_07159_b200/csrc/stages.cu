@@ -3,6 +3,7 @@
 // Each call uploads its host inputs, runs the SAME kernels the batched
 // pipeline runs (B = 1), and downloads the result. Tests compare these, stage
 // by stage, with the CPU oracle on identical inputs.
+#include <cmath>
 #include "hwflow_c.h"
 #include "host.h"
 
@@ -275,6 +276,142 @@ int hwf_linearize(hwf_ctx* ctx, const hwf_level* lv, const hwf_energy_params* P,
     down(sys.data(), d.sys, sys.size());
     unpack_system(d.gw, d.gh, sys, blocks, rhs, precond);
   });
+}
+
+// assemble_jacobian (solver.cpp:247-314): the device evaluates eval_pixel / eval_node with derivatives (the
+// LIN kernels' test-hook dumps); the host lays the values out as the reference's triplets, in its loop order.
+int hwf_assemble_jacobian(hwf_ctx* ctx, const hwf_level* lv, const hwf_energy_params* P, uint32_t active,
+                          int negate_field, double* residuals, int* rows, int* cols, double* vals, long long cap,
+                          long long* nnz) {
+  return guard(ctx, [&] {
+    if (!lv || !P || !nnz || negate_field < -1 || negate_field > 2) throw InvalidArg("bad jacobian query");
+    if (P->w_epi > 0.0 && !lv->fundamental) throw InvalidArg("epipolar term enabled without a fundamental matrix");
+    DevMem m;
+    LevelDev d;
+    load_level(m, d, lv, false, 0, ctx->stream);
+    const double* dF = lv->fundamental ? up(m, lv->fundamental, 9) : nullptr;
+    Energies E;
+    make_energies(m, E, d, 1);
+    int* flags = up<int>(m, nullptr, 1);
+    const size_t N = d.N, G = d.G;
+    double* pj = m.alloc<double>(14 * N);
+    double* nj = m.alloc<double>(kNodeJac * G);
+    PixArgs pa = pix_args(d, P, active, flags, E);
+    pa.refresh = 0;
+    pa.jac = pj;
+    launch_pixel(true, pa, 1, ctx->stream);
+    NodeArgs na = node_args(d, P, active, 0.0, dF, flags, E);
+    na.refresh = 0;
+    na.jac = nj;
+    launch_node(true, na, 1, ctx->stream);
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaGetLastError());
+    check_flags(flags);
+    std::vector<double> hp(14 * N), hn(kNodeJac * G);
+    down(hp.data(), pj, hp.size());
+    down(hn.data(), nj, hn.size());
+    std::vector<int> R0, C0;
+    std::vector<double> V0;
+    const long long M = 2 * static_cast<long long>(N) + 14 * static_cast<long long>(G);
+    std::vector<double> R(static_cast<size_t>(M), 0.0);
+    auto push = [&](int r, int c, double v) {
+      R0.push_back(r);
+      C0.push_back(c);
+      V0.push_back(v);
+    };
+    auto hooks = [&](double* v) {  // mask_fields, then the negative control
+      for (int f = 0; f < 3; ++f)
+        if (!((active >> f) & 1)) v[2 * f] = v[2 * f + 1] = 0.0;
+      if (negate_field >= 0) {
+        v[2 * negate_field] *= -1.0;
+        v[2 * negate_field + 1] *= -1.0;
+      }
+    };
+    const int w = d.w, step = d.step, gw = d.gw, gh = d.gh, Ni = static_cast<int>(N), Gi = static_cast<int>(G);
+    for (int pix = 0; pix < Ni; ++pix) {
+      const double* e = &hp[14 * static_cast<size_t>(pix)];
+      R[pix] = e[0];
+      R[Ni + pix] = e[1];
+      double jp[6], jg[6];
+      for (int j = 0; j < 6; ++j) {
+        jp[j] = e[2 + j];
+        jg[j] = e[8 + j];
+      }
+      hooks(jp);
+      hooks(jg);
+      // WarpGrid::support (warp_grid.cpp:41-54)
+      const double u = static_cast<double>(pix % w) / step, v = static_cast<double>(pix / w) / step;
+      const int a0 = std::min(std::max(static_cast<int>(std::floor(u)), 0), gw - 2);
+      const int b0 = std::min(std::max(static_cast<int>(std::floor(v)), 0), gh - 2);
+      const double fu = std::min(std::max(u - a0, 0.0), 1.0), fv = std::min(std::max(v - b0, 0.0), 1.0);
+      const int node[4] = {b0 * gw + a0, b0 * gw + a0 + 1, (b0 + 1) * gw + a0, (b0 + 1) * gw + a0 + 1};
+      const double wt[4] = {(1 - fu) * (1 - fv), fu * (1 - fv), (1 - fu) * fv, fu * fv};
+      for (int i = 0; i < 4; ++i) {
+        if (wt[i] == 0.0) continue;
+        for (int j = 0; j < 6; ++j) {
+          const int col = 6 * node[i] + j;
+          if (jp[j] != 0.0) push(pix, col, wt[i] * jp[j]);
+          if (jg[j] != 0.0) push(Ni + pix, col, wt[i] * jg[j]);
+        }
+      }
+    }
+    for (int n = 0; n < Gi; ++n) {
+      const double* e = &hn[kNodeJac * static_cast<size_t>(n)];
+      const int right = (n % gw + 1 < gw) ? n + 1 : -1, down_ = (n / gw + 1 < gh) ? n + gw : -1;
+      for (int row = 0; row < 6; ++row) {
+        const int r = 2 * Ni + 6 * n + row;
+        R[r] = e[row];
+        const int f = row / 2;
+        if (!((active >> f) & 1)) continue;
+        const double sgn = f == negate_field ? -1.0 : 1.0;
+        if (e[6 + row] != 0.0) push(r, 6 * n + row, sgn * e[6 + row]);
+        if (right >= 0 && e[12 + row] != 0.0) push(r, 6 * right + row, sgn * e[12 + row]);
+        if (down_ >= 0 && e[18 + row] != 0.0) push(r, 6 * down_ + row, sgn * e[18 + row]);
+      }
+      for (int t = 0; t < 2; ++t) {
+        const int r = 2 * Ni + 6 * Gi + 2 * n + t;
+        R[r] = e[24 + t];
+        double j[6];
+        for (int c = 0; c < 6; ++c) j[c] = e[26 + 6 * t + c];
+        hooks(j);
+        for (int c = 0; c < 6; ++c)
+          if (j[c] != 0.0) push(r, 6 * n + c, j[c]);
+      }
+      for (int row = 0; row < 6; ++row) {
+        const int r = 2 * Ni + 8 * Gi + 6 * n + row;
+        R[r] = e[38 + row];
+        const int f = row / 2;
+        if (!((active >> f) & 1)) continue;
+        const double sgn = f == negate_field ? -1.0 : 1.0;
+        if (e[44 + row] != 0.0) push(r, 6 * n + row, sgn * e[44 + row]);
+      }
+    }
+    *nnz = static_cast<long long>(V0.size());
+    if (residuals) std::copy(R.begin(), R.end(), residuals);
+    if (cap > 0 || rows || cols || vals) {
+      if (cap < *nnz || !rows || !cols || !vals) throw InvalidArg("jacobian triplet buffers too small");
+      std::copy(R0.begin(), R0.end(), rows);
+      std::copy(C0.begin(), C0.end(), cols);
+      std::copy(V0.begin(), V0.end(), vals);
+    }
+  });
+}
+
+int hwf_normal_dense(int gw, int gh, const double* blocks, double* dense) {  // solver.cpp:89-98
+  if (gw < 1 || gh < 1 || !blocks || !dense) return HWF_EINVAL;
+  const long long G = static_cast<long long>(gw) * gh, D = 6 * G;
+  std::fill(dense, dense + D * D, 0.0);
+  for (long long n = 0; n < G; ++n)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        const long long a = n % gw + dx, b = n / gw + dy;
+        if (a < 0 || a >= gw || b < 0 || b >= gh) continue;
+        const long long nb = b * gw + a;
+        const double* B = blocks + (n * 9 + (dy + 1) * 3 + (dx + 1)) * 36;
+        for (int i = 0; i < 6; ++i)
+          for (int j = 0; j < 6; ++j) dense[(6 * n + i) * D + 6 * nb + j] = B[6 * i + j];
+      }
+  return HWF_OK;
 }
 
 int hwf_pcg(hwf_ctx* ctx, int gw, int gh, const double* blocks, const double* rhs, int iters, double* x_out,

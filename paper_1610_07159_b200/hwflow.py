@@ -409,6 +409,34 @@ class Solver:
                                               dptr(blocks), dptr(rhs), dptr(pre)))
         return blocks, rhs, pre
 
+    def assemble_jacobian(self, lv: LevelState, params: EnergyParams, active_fields: int = 7, negate_field: int = -1):
+        """assemble_jacobian (solver.hpp:106-111, solver.cpp:247-314): (R, rows, cols, vals), the stacked residuals
+        (M = 2N + 14G) and dR/dx as triplets in the reference's order; negate_field flips one flow field's analytic
+        derivatives (the negative-control hook)."""
+        c, pc = lv.to_c(), params.to_c()
+        gw, gh = grid_dims(lv.width, lv.height, lv.grid_step)
+        R = np.empty(2 * lv.width * lv.height + 14 * gw * gh)
+        nnz = C.c_longlong()
+        self.ctx.check(self.lib.hwf_assemble_jacobian(self.ctx.h, C.byref(c), C.byref(pc), active_fields, negate_field,
+                                                      dptr(None), None, None, dptr(None), 0, C.byref(nnz)))
+        n = nnz.value
+        rows, cols, vals = np.empty(n, np.int32), np.empty(n, np.int32), np.empty(n)
+        ip = C.POINTER(C.c_int)
+        self.ctx.check(self.lib.hwf_assemble_jacobian(self.ctx.h, C.byref(c), C.byref(pc), active_fields, negate_field,
+                                                      dptr(R), rows.ctypes.data_as(ip), cols.ctypes.data_as(ip),
+                                                      dptr(vals), n, C.byref(nnz)))
+        return R, rows, cols, vals
+
+    def normal_dense(self, gw: int, gh: int, blocks: np.ndarray) -> np.ndarray:
+        """NormalSystem::dense (solver.hpp:77, solver.cpp:89-98) of a system in hwf_linearize layout."""
+        b = np.ascontiguousarray(blocks, np.float64)
+        D = 6 * gw * gh
+        out = np.empty((D, D))
+        rc = self.lib.hwf_normal_dense(gw, gh, dptr(b), dptr(out))
+        if rc != capi.HWF_OK:
+            raise ValueError("hwf_normal_dense: bad arguments")
+        return out
+
     def pcg_solve(self, gw: int, gh: int, blocks: np.ndarray, rhs: np.ndarray, iters: int, trace: bool = False):
         b, r = np.ascontiguousarray(blocks, np.float64), np.ascontiguousarray(rhs, np.float64)
         x = np.empty(6 * gw * gh)

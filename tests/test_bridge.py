@@ -38,6 +38,8 @@ def test_bridge_runs_reference_api_on_device(oracle, tmp_path):
     # SolverDivergence (core.hpp:19) / std::invalid_argument (energy.cpp:43-50) thrown where the reference throws
     assert d["divergence_dev"] == d["divergence_ref"], d
     assert d["invalid_ref"] == 2 and d["invalid_dev"] == 2
+    # assemble_jacobian (solver.cpp:247-314) with the negate_field hook: the reference's triplets, in order
+    assert d["jacobian_same_entries"] is True and d["jacobian_nnz"] > 0 and d["jacobian_rel"] < 1e-9
     # run_scene_flow through the bridge vs the oracle's Algorithm 1 on the same images
     w, h = d["solve_width"], d["solve_height"]
     N = w * h
