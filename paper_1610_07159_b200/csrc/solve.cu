@@ -234,6 +234,9 @@ struct alignas(16) Swz22Smem {
 // a / b for the PCG step lengths: the hardware reciprocal estimate refined by two Newton steps
 // (error ~1 ulp against the correctly rounded quotient; no libdevice slow-path branch)
 __device__ __forceinline__ double fdiv(double a, double b) {
+#ifdef HWF_EXACT_MATH
+  return a / b;
+#endif
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
   double e = __fma_rn(-b, r, 1.0);
