@@ -261,6 +261,27 @@ __device__ __forceinline__ void warp_pos_exact(double x, double y, const double 
   wy = __dadd_rn(__dadd_rn(__dadd_rn(y, sc * f[1]), st * f[3]), scst * f[5]);
 }
 
+// One occlusion lattice vertex (pin C.2, oracle/hierarchy.cpp) from the exactly interpolated flow fl at halfway
+// pixel (x, y): its position in the 4 views in 1/256 px fixed point, the float depth proxy 1/(|2s| + 1e-3), and
+// validity. Written by k_occ_project, or by the fused E_after pass (k_pixel<false, *, *, *, PROJ>).
+__device__ __forceinline__ bool occ_project_flow(int x, int y, const double fl[6], int2 (&q)[4], float& zf) {
+  const double s2x = 2.0 * fl[0], s2y = 2.0 * fl[1];
+  const double nrm = __dsqrt_rn(__dadd_rn(__dmul_rn(s2x, s2x), __dmul_rn(s2y, s2y)));
+  const double z = __ddiv_rn(1.0, __dadd_rn(nrm, 1e-3));
+  zf = __double2float_rn(z);
+  bool ok = isfinite(z);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    double wx, wy;
+    warp_pos_exact(x, y, fl, e, wx, wy);
+    const double fx = wx * 256.0, fy = wy * 256.0;
+    ok = ok && isfinite(fx) && isfinite(fy) && fabs(fx) < 1073741824.0 && fabs(fy) < 1073741824.0;
+    q[e].x = ok ? static_cast<int>(__double2ll_rn(fx)) : 0;
+    q[e].y = ok ? static_cast<int>(__double2ll_rn(fy)) : 0;
+  }
+  return ok;
+}
+
 // deterministic warp sum (xor butterfly: every lane ends with the identical value)
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -274,9 +274,13 @@ inline double* swept(LevelDev& d, int s) { return s & 1 ? d.xa : d.xb; }
 // E_after of the last iteration (solver.cpp:523-528).
 inline void rec_energy_after(LevelDev& d, int B, const hwf_energy_params& P, const hwf_schedule& S, const double* dF,
                              int gn, const Energies& E, int slot_base, int* flags, cudaStream_t st, Launches& L,
-                             const uint8_t* src8, const Range* R = nullptr) {
+                             const uint8_t* src8, const Range* R = nullptr, int2* occ_q = nullptr,
+                             float* occ_z = nullptr, uint8_t* occ_bad = nullptr) {
   PixArgs pa = pixel_args(d, P, S, src8, flags, E, R);
   pa.refresh = 0;
+  pa.occ_q = occ_q;  // non-null: also write the level's occlusion vertices (k_occ_project's work)
+  pa.occ_z = occ_z;
+  pa.occ_bad = occ_bad;
   pa.ep_new = E.slot(slot_base + 2 * (gn - 1) + 1);
   pa.ep_old = nullptr;
   if (R && !R->whole) {  // energies only: the owned rows
@@ -346,8 +350,6 @@ struct Plan {
   double* o_slot[2][4] = {{nullptr, nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr, nullptr}};  // streaming
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
-  cudaStream_t side = nullptr;  // capture-time branch for the per-level E_after pass
-  cudaEvent_t fork_ev[HWF_MAX_LEVELS] = {}, join_ev[HWF_MAX_LEVELS] = {};
   // streaming (hwf_submit_batch / hwf_wait): two input/result slots, one graph each
   bool async_ready = false;
   void* in_slot[2] = {};
@@ -373,11 +375,6 @@ struct Plan {
     return !F_ || std::memcmp(F, F_, sizeof(F)) == 0;
   }
   ~Plan() {
-    if (side) cudaStreamDestroy(side);
-    for (int l = 0; l < HWF_MAX_LEVELS; ++l) {
-      if (fork_ev[l]) cudaEventDestroy(fork_ev[l]);
-      if (join_ev[l]) cudaEventDestroy(join_ev[l]);
-    }
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
     if (exec_slot[1]) cudaGraphExecDestroy(exec_slot[1]);
@@ -529,26 +526,20 @@ struct Plan {
       LC.ev = &ev;
       LC.bytes = &ev_bytes;
     }
-    if (!side) {
-      CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-      for (int l = 0; l < L; ++l) {
-        CK(cudaEventCreateWithFlags(&fork_ev[l], cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&join_ev[l], cudaEventDisableTiming));
-      }
-    }
     rec_prologue(st, LC);
     for (int l = L - 1; l >= 0; --l) {
       rec_level_begin(l, st, LC);
       record_gn_level(lv[l], B, P, S, dF, gn[l], E, slot_base[l], sc, flags, st, LC, src8(l), false);
-      // E_after of the level's last iteration only feeds the stats: a graph branch beside the
-      // occlusion and illumination of the same level (which do not touch its inputs)
-      CK(cudaEventRecord(fork_ev[l], st));
-      CK(cudaStreamWaitEvent(side, fork_ev[l], 0));
-      if (gn[l] > 0) rec_energy_after(lv[l], B, P, S, dF, gn[l], E, slot_base[l], flags, side, LC, src8(l));
-      CK(cudaEventRecord(join_ev[l], side));
-      rec_level_end(l, st, LC);
+      if (gn[l] > 0) {
+        // E_after of the level's last iteration (stats) fused with the occlusion projection of the same flow:
+        // one pass interpolates the final flow per pixel for both, then raster/resolve and illumination
+        rec_energy_after(lv[l], B, P, S, dF, gn[l], E, slot_base[l], flags, st, LC, src8(l), nullptr, sc.q, sc.Z,
+                         sc.bad);
+        rec_level_end(l, st, LC, true);
+      } else {
+        rec_level_end(l, st, LC);
+      }
     }
-    for (int l = 0; l < L; ++l) CK(cudaStreamWaitEvent(st, join_ev[l], 0));
     rec_epilogue(st, LC);
     launches = LC.count;
   }
@@ -599,11 +590,16 @@ struct Plan {
   }
 
   // occlusion and illumination of the solved level
-  void rec_level_end(int l, cudaStream_t st, Launches& LC) {
+  void rec_level_end(int l, cudaStream_t st, Launches& LC, bool projected = false) {
     LevelDev& d = lv[l];
-    launch_occlusion(d.w, d.h, d.gw, d.gh, d.step, d.total, B, sc.q, sc.Z, sc.bad, sc.zbuf, sc.degen, sc.queue,
-                     sc.qcount, d.occ, st);
-    LC.count += 4;
+    if (projected) {  // the vertices were written by the fused E_after pass
+      launch_occlusion_projected(d.w, d.h, B, sc.q, sc.Z, sc.bad, sc.zbuf, sc.degen, sc.queue, sc.qcount, d.occ, st);
+      LC.count += 3;
+    } else {
+      launch_occlusion(d.w, d.h, d.gw, d.gh, d.step, d.total, B, sc.q, sc.Z, sc.bad, sc.zbuf, sc.degen, sc.queue,
+                       sc.qcount, d.occ, st);
+      LC.count += 4;
+    }
     if (l > 0) {
       launch_illumination(d.w, d.h, d.gw, d.gh, d.step, d.img, d.total, d.occ, B, sc.resid, sc.tmp, d.hm, st);
       LC.count += 3;

@@ -43,6 +43,10 @@ struct PixArgs {
   // contribute energy partials (others write zeros); ty1 <= 0 = the whole level
   int ty0, ty1, own0, own1;
   double* jac;          // test hook (hwf_assemble_jacobian, LIN): per pixel {r_p, r_g, J_p[6], J_g[6]}, or null
+  // E_after pass fused with the occlusion projection (k_occ_project's outputs), or null
+  int2* occ_q;
+  float* occ_z;
+  uint8_t* occ_bad;
 };
 
 struct NodeArgs {
@@ -145,6 +149,9 @@ void launch_init_coarse(double* base, double* total, double* delta, int G, int B
 void launch_occlusion(int w, int h, int gw, int gh, int step, const double* total, int B,
                       int2* q, float* Z, uint8_t* bad, unsigned long long* zbuf, uint8_t* degen,
                       unsigned long long* queue, unsigned int* qcount, uint8_t* vis_out, cudaStream_t s);
+void launch_occlusion_projected(int w, int h, int B, int2* q, float* Z, uint8_t* bad, unsigned long long* zbuf,
+                                uint8_t* degen, unsigned long long* queue, unsigned int* qcount, uint8_t* vis_out,
+                                cudaStream_t s);
 void launch_illumination(int w, int h, int gw, int gh, int step, const double* img,
                          const double* total, const uint8_t* vis, int B, double* resid,
                          double* tmp, double* hm, cudaStream_t s);

@@ -92,22 +92,12 @@ __global__ void k_occ_project(int w, int h, int gw, int gh, int step, const doub
   const size_t pix = static_cast<size_t>(y) * w + x;
   double fl[6];
   interp_exact(total + pair * G * 6, gw, gh, step, x, y, fl);
-  const double s2x = 2.0 * fl[0], s2y = 2.0 * fl[1];
-  const double nrm = __dsqrt_rn(__dadd_rn(__dmul_rn(s2x, s2x), __dmul_rn(s2y, s2y)));
-  const double z = __ddiv_rn(1.0, __dadd_rn(nrm, 1e-3));
-  Z[pair * N + pix] = __double2float_rn(z);
-  bool ok = isfinite(z);
+  int2 v[4];
+  float zf;
+  const bool ok = occ_project_flow(x, y, fl, v, zf);
+  Z[pair * N + pix] = zf;
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    double wx, wy;
-    warp_pos_exact(x, y, fl, e, wx, wy);
-    const double fx = wx * 256.0, fy = wy * 256.0;
-    ok = ok && isfinite(fx) && isfinite(fy) && fabs(fx) < 1073741824.0 && fabs(fy) < 1073741824.0;
-    int2 v;
-    v.x = ok ? static_cast<int>(__double2ll_rn(fx)) : 0;
-    v.y = ok ? static_cast<int>(__double2ll_rn(fy)) : 0;
-    q[(pair * 4 + e) * N + pix] = v;  // view-major: a triangle's vertices are contiguous
-  }
+  for (int e = 0; e < 4; ++e) q[(pair * 4 + e) * N + pix] = v[e];  // view-major: a triangle's vertices are contiguous
   bad[pair * N + pix] = ok ? 0 : 1;
 }
 
@@ -580,8 +570,14 @@ void launch_init_coarse(double* base, double* total, double* delta, int G, int B
 void launch_occlusion(int w, int h, int gw, int gh, int step, const double* total, int B, int2* q, float* Z,
                       uint8_t* bad, unsigned long long* zbuf, uint8_t* degen, unsigned long long* queue,
                       unsigned int* qcount, uint8_t* vis_out, cudaStream_t s) {
-  const size_t N = static_cast<size_t>(w) * h;
   k_occ_project<<<rows_grid(w, h, B), kThreads, 0, s>>>(w, h, gw, gh, step, total, q, Z, bad);
+  launch_occlusion_projected(w, h, B, q, Z, bad, zbuf, degen, queue, qcount, vis_out, s);
+}
+// raster + resolve from vertices already projected (by k_occ_project or the fused E_after pass)
+void launch_occlusion_projected(int w, int h, int B, int2* q, float* Z, uint8_t* bad, unsigned long long* zbuf,
+                                uint8_t* degen, unsigned long long* queue, unsigned int* qcount, uint8_t* vis_out,
+                                cudaStream_t s) {
+  const size_t N = static_cast<size_t>(w) * h;
   if (w >= 2 && h >= 2) {
     cudaMemsetAsync(zbuf, 0xFF, N * 4 * B * sizeof(unsigned long long), s);
     cudaMemsetAsync(qcount, 0, sizeof(unsigned int), s);
