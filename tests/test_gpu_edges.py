@@ -26,8 +26,10 @@ STAGE_RTOL = 1e-9
 FLOW_TOL_PX = 1e-3
 ENERGY_RTOL = 1e-4
 
+# (65, 49, 8) and (641, 481, 8): (w - 1) and (h - 1) divisible by the step, so the last cell holds step + 1
+# pixels and the last k_pixel tiles are 17 x 17 (the largest tile that keeps the 27-product records)
 SHAPES = [(2, 2, 1), (3, 5, 1), (17, 13, 3), (41, 9, 5), (200, 3, 7), (65, 33, 16), (70, 70, 32), (5, 120, 2),
-          (1, 9, 2), (9, 1, 4)]
+          (1, 9, 2), (9, 1, 4), (65, 49, 8), (641, 481, 8)]
 
 
 def _level(seed, w, h, step):
@@ -60,7 +62,8 @@ def test_stage_seams_on_ragged_shapes(device, oracle, w, h, step):
         np.testing.assert_allclose(pa, pb, rtol=1e-7, atol=1e-12 * max(np.abs(pb).max(), 1e-300))
 
 
-@pytest.mark.parametrize("w,h,step,sub", [(18, 14, 1, 0), (33, 17, 3, 0), (100, 20, 5, 0), (47, 61, 2, 16),
+@pytest.mark.parametrize("w,h,step,sub", [(18, 14, 1, 0), (33, 17, 3, 0), (100, 20, 5, 0), (65, 49, 8, 0),
+                                          (47, 61, 2, 16),
                                           (47, 61, 3, 16), (96, 64, 4, 8), (96, 64, 16, 16), (130, 70, 32, 16)])
 def test_solve_on_ragged_shapes(device, oracle, w, h, step, sub):
     imgs = synthetic.render_pair(w, h, s=(1.5, 0.0), m=(0.5, 0.25), seed=w + h, dtype=np.float64)
