@@ -9,8 +9,10 @@ Collectives and data movement per frame:
   - Schwarz mode, after every sweep but the last: halo exchange of the published x rows next
     to each strip (P2P), 2 node rows per rank.
   - Global-PCG mode (the headline schedule), per PCG iteration: two all-gathers of the dot
-    partials (each rank's tiles, a few hundred KB at 4K) and one z halo exchange; every rank
-    then sums the same partials in the same order, so the scalars agree bitwise.
+    partials (each rank's tiles, a few hundred KB at 4K); every rank then sums the same
+    partials in the same order, so the scalars agree bitwise. The z halo the next spmv needs
+    rides in the second gather's buffer (each rank appends its first and last z rows), so it
+    costs no collective of its own.
   - After every Gauss-Newton iteration: all-gather of the owned total/delta rows. Occlusion,
     illumination, prolongation and the next linearisation read the whole grid.
   - At the end: sum-all-reduce of the energy partials and OR of the divergence flags.
@@ -182,6 +184,11 @@ class LocalComm:
                     if dst is not src:
                         dst.buffer(level, name)[sl].copy_(src.buffer(level, name)[sl])
 
+    def allgather_rows_halo(self, ranks: list[SplitRank], level: int, name: str, halo_name: str):
+        """allgather_rows(name) and halo(halo_name) as one exchange (TorchComm fuses them)."""
+        self.allgather_rows(ranks, level, name)
+        self.halo(ranks, level, halo_name)
+
     def allreduce_sum(self, ranks: list[SplitRank], name: str):
         with self._streamed(ranks):
             bufs = [r.buffer(0, name) for r in ranks]
@@ -267,6 +274,39 @@ class TorchComm:
                 if r != me.rank and b > a:
                     buf[me.row_slice(level, a, b, name)].copy_(out[r * span: r * span + w * (b - a)])
 
+    def allgather_rows_halo(self, ranks: list[SplitRank], level: int, name: str, halo_name: str):
+        """One all-gather carries both: every rank's `name` rows, then its first and last `halo_name` rows.
+        Strips are contiguous, so the halo row above a strip is its owner's last row and the one below is
+        its owner's first; the P2P exchange of halo() is folded into the collective the protocol already
+        makes (the PCG's partial-sum gather)."""
+        (me,) = ranks
+        rows = [self.table[r][level] for r in range(self.world)]
+        w, wh = me.row_elems(level, name), me.row_elems(level, halo_name)
+        span = w * max(n1 - n0 for n0, n1 in rows)
+        if span == 0:
+            return
+        buf, hb = me.buffer(level, name), me.buffer(level, halo_name)
+        gh = max(n1 for _, n1 in rows)
+        n0, n1 = rows[me.rank]
+        with self._streamed(ranks):
+            slab = torch.zeros(span + 2 * wh, dtype=buf.dtype, device=buf.device)
+            if n1 > n0:
+                slab[: w * (n1 - n0)].copy_(buf[me.row_slice(level, n0, n1, name)])
+                slab[span: span + wh].copy_(hb[me.row_slice(level, n0, n0 + 1, halo_name)])
+                slab[span + wh:].copy_(hb[me.row_slice(level, n1 - 1, n1, halo_name)])
+            stride = span + 2 * wh
+            out = torch.empty(self.world * stride, dtype=buf.dtype, device=buf.device)
+            dist.all_gather_into_tensor(out, slab, group=self.group)
+            for r, (a, b) in enumerate(rows):
+                if r != me.rank and b > a:
+                    buf[me.row_slice(level, a, b, name)].copy_(out[r * stride: r * stride + w * (b - a)])
+            if n1 > n0:
+                for q in (n0 - 1, n1):
+                    if 0 <= q < gh:
+                        o = _owner(rows, q)
+                        at = o * stride + span + (0 if q == rows[o][0] else wh)
+                        hb[me.row_slice(level, q, q + 1, halo_name)].copy_(out[at: at + wh])
+
     def allreduce_sum(self, ranks: list[SplitRank], name: str):
         (me,) = ranks
         with self._streamed(ranks):
@@ -298,20 +338,20 @@ def _frame(images: np.ndarray) -> tuple[Frame4C, np.ndarray]:
 
 def _pcg_split(ranks: list[SplitRank], comm, l: int):
     """pcg_solve (solver.cpp:365-380) across the strips, include/hwflow_split.h's protocol."""
-    def phase(ph: int, it: int = 0):
+    def phase(ph: int, it: int = 0, z_halo: bool = False):
         for r in ranks:
             r.pcg(l, ph, it)
-        comm.allgather_rows(ranks, l, "pcg_part")
+        if z_halo:  # phases 0 and 2 leave z for the next spmv: its halo rides on the partials' gather
+            comm.allgather_rows_halo(ranks, l, "pcg_part", "z")
+        else:
+            comm.allgather_rows(ranks, l, "pcg_part")
         for r in ranks:
             r.pcg_scalars(l, ph, it)
 
-    phase(0)
-    comm.halo(ranks, l, "z")
+    phase(0, z_halo=True)
     for it in range(ranks[0].pcg_iters):
         phase(1, it)
-        phase(2, it)
-        if it < ranks[0].pcg_iters - 1:
-            comm.halo(ranks, l, "z")
+        phase(2, it, z_halo=it < ranks[0].pcg_iters - 1)
 
 
 def _split_body(ranks: list[SplitRank], comm):

@@ -86,6 +86,9 @@ class NullComm(LocalComm):
     def allgather_rows(self, *a):
         pass
 
+    def allgather_rows_halo(self, *a):
+        pass
+
     def allreduce_sum(self, *a):
         pass
 
@@ -131,6 +134,13 @@ class CountingComm(LocalComm):
         self.gather_bytes += w * gh * 8  # every rank receives the whole buffer
         self.gathers += 1
         super().allgather_rows(ranks, level, name)
+
+    def allgather_rows_halo(self, ranks, level, name, halo_name):
+        """One collective (TorchComm folds the halo rows into the gather)."""
+        h, hb = self.halos, self.halo_bytes
+        super().allgather_rows_halo(ranks, level, name, halo_name)
+        self.halos = h
+        self.halo_bytes = hb + 2 * ranks[0].row_elems(level, halo_name) * 8 * len(ranks)
 
 
 def main():
