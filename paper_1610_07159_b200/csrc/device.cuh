@@ -21,7 +21,14 @@
 
 namespace hwf {
 
-constexpr int kCellStride = 234;
+// per-cell records of k_pixel's reduction: 10 corner-pair blocks of 21 packed entries, then 4 corner rhs of 6
+#ifdef HWF_CELLS_PAD  // blocks padded to 22 doubles: 16 B aligned, k_node reads them as double2
+constexpr int kCellBlk = 22;
+#else
+constexpr int kCellBlk = 21;
+#endif
+constexpr int kCellRhs = 10 * kCellBlk;
+constexpr int kCellStride = kCellRhs + 24;
 constexpr int kSysStride = 120;
 constexpr int kSysRhs = 105;
 constexpr int kSysPre = 111;
@@ -36,6 +43,9 @@ __host__ __device__ __forceinline__ int sym6(int i, int j) {
   }
   return i * 6 - (i * (i - 1)) / 2 + (j - i);
 }
+// (i, j) of packed index m (the inverse of sym6)
+__host__ __device__ constexpr int sym_i(int m) { return m < 6 ? 0 : (m < 11 ? 1 : (m < 15 ? 2 : (m < 18 ? 3 : (m < 20 ? 4 : 5)))); }
+__host__ __device__ constexpr int sym_j(int m) { return m - (sym_i(m) * 6 - (sym_i(m) * (sym_i(m) - 1)) / 2) + sym_i(m); }
 // unordered corner pair (i <= j) of a cell, 10 pairs
 __host__ __device__ __forceinline__ int pair4(int i, int j) {
   if (i > j) {

@@ -1,6 +1,6 @@
 """Per-source-line and per-opcode breakdown of one kernel in an ncu report (run here, no GPU).
 
-    python tools/ncu_lines.py report.ncu-rep [--top 40]
+    python tools/ncu_lines.py report.ncu-rep [--top 40] [--op IMAD]
 
 Reads `ncu --page source --print-source cuda,sass --csv` and sums, per CUDA source line, the warp-level
 instructions executed, the stall samples, and the FP64 / shared / local instructions; plus a per-opcode table.
@@ -14,6 +14,8 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[sys.argv.index("--top") + 1]) if "--top" in sys.argv else 40
+want_op = sys.argv[sys.argv.index("--op") + 1] if "--op" in sys.argv else None
+by_op = collections.Counter()  # (line, full opcode) -> instructions, for --op
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 lines = collections.defaultdict(lambda: collections.Counter())
@@ -60,6 +62,8 @@ for row in csv.reader(io.StringIO(out)):
         c["local"] += ie
     ops[op] += ie
     opsamp[op] += smp
+    if op == want_op:
+        by_op[(cur, body.split(None, 1)[0])] += ie
 tot = sum(c["inst"] for c in lines.values())
 tsm = sum(c["samples"] for c in lines.values())
 print(f"total warp instructions {tot:.4g}, stall samples {tsm:.4g}")
@@ -70,3 +74,7 @@ for key, c in sorted(lines.items(), key=lambda kv: -kv[1]["samples"])[:top]:
 print("\nopcode            inst%   samp%")
 for op, v in ops.most_common(30):
     print(f"{op:16s} {100*v/tot:6.2f} {100*opsamp[op]/tsm:6.2f}")
+if want_op:
+    print(f"\n{want_op} by source line (full opcode), share of all instructions")
+    for (key, full), v in by_op.most_common(top):
+        print(f"{key[0][:14]}:{key[1]:<6d} {full:22s} {100*v/tot:6.2f}  {src_text[key]}")
