@@ -22,13 +22,15 @@
 namespace hwf {
 
 // per-cell records of k_pixel's reduction: 10 corner-pair blocks of 21 packed entries, then 4 corner rhs of 6
-#ifdef HWF_CELLS_PAD  // blocks padded to 22 doubles: 16 B aligned, k_node reads them as double2
-constexpr int kCellBlk = 22;
-#else
-constexpr int kCellBlk = 21;
+#ifdef HWF_CELLS_PACKED  // A/B: packed blocks (21 and 6 doubles), 8 B aligned
+constexpr int kCellBlk = 21, kCellRhsW = 6;
+#else  // blocks padded to 24 doubles and rhs to 8: 32 B aligned, so k_node reads whole sectors (256-bit loads)
+#define HWF_CELLS_V4
+constexpr int kCellBlk = 24, kCellRhsW = 8;
 #endif
 constexpr int kCellRhs = 10 * kCellBlk;
-constexpr int kCellStride = kCellRhs + 24;
+constexpr int kCellStride = kCellRhs + 4 * kCellRhsW;
+constexpr int kCellData = 10 * 21 + 4 * 6;  // the doubles of a cell record that carry data (algorithmic bytes)
 constexpr int kSysStride = 120;
 constexpr int kSysRhs = 105;
 constexpr int kSysPre = 111;

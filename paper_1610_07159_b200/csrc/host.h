@@ -182,7 +182,7 @@ inline double pixel_bytes(const LevelDev& d, int B, bool illum, bool u8) {
   // 4 images (32 B {v, gx, gy, 0} sample texels read with one 256-bit load, or the u8 frames at the finest
   // level), illumination (2 coarse half maps, one value per 2x2 pixels), vis4 + W in/out, halfway out
   const double perpix = 4 * (u8 ? 1.0 : 32.0) + (illum ? 2 * 8.0 / 4.0 : 0.0) + 1 + 1 + 1 + 8;
-  return B * (d.N * perpix + d.G * 48.0 + d.C * kCellStride * 8.0);
+  return B * (d.N * perpix + d.G * 48.0 + d.C * kCellData * 8.0);
 }
 
 // Rows of one level a strip-split rank works on (hwflow_split.h); whole = the level.
