@@ -88,6 +88,28 @@ struct Coord {
 };
 __device__ __forceinline__ Coord cell_coord(double v, int n) {
   Coord c;
+#if defined(HWF_CELL_COORD) && HWF_CELL_COORD > 0  // A/B (tools/cell_coord_ab.py): branch-free forms
+  const bool lo = v <= 0.0, hi = v >= n - 1;  // both false for NaN
+  const double fl = floor(v);
+#if HWF_CELL_COORD == 1  // the same function with selects: NaN keeps f = NaN, i0 = (int)NaN = 0
+  c.i0 = lo ? 0 : (hi ? (n >= 2 ? n - 2 : 0) : static_cast<int>(fl));
+  c.f = lo ? 0.0 : (hi ? 1.0 : v - fl);
+#elif HWF_CELL_COORD == 2  // clamp first with fmin/fmax: a NaN coordinate becomes 0 (cell 0, f = 0)
+  const double vc = fmin(fmax(v, 0.0), static_cast<double>(n - 1));
+  c.i0 = min(static_cast<int>(floor(vc)), max(n - 2, 0));
+  c.f = vc - c.i0;
+#else  // 3: the cell clamped but not the fraction (f = v - i0 extrapolates outside [0, n - 1])
+  c.i0 = min(max(static_cast<int>(fl), 0), max(n - 2, 0));
+  c.f = v - c.i0;
+#endif
+  c.clamped = lo || hi;
+  if (n == 1) {
+    c.i0 = 0;
+    c.f = 0.0;
+    c.clamped = true;
+  }
+  return c;
+#endif
   if (v <= 0.0) {
     c.i0 = 0;
     c.f = 0.0;
