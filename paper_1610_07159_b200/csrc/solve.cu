@@ -618,10 +618,15 @@ __device__ __forceinline__ double tile_spmv(const PcgArgs& a, const PcgPtr& P, c
   };
   double A[2][21];
   bool vb[9];
+#ifdef HWF_DIAG_SPMV_FWD_ONLY  // diagnostic A/B only (wrong results): the 5 forward slots, no backward blocks
+  constexpr int s9_first = 4;
+#else
+  constexpr int s9_first = 0;
+#endif
   {
-    const double* b0 = block(0, vb[0]);
+    const double* b0 = block(s9_first, vb[s9_first]);
 #pragma unroll
-    for (int m = 0; m < 21; ++m) A[0][m] = __ldg(b0 + m * P.G);
+    for (int m = 0; m < 21; ++m) A[s9_first & 1][m] = __ldg(b0 + m * P.G);
   }
   // stage p_next = z + beta p_prev, rows b-1..b+1 x nodes a0-1 .. a0+width (6 (width + 2) contiguous
   // doubles per row), all of a row's loads issued before its stores
@@ -667,7 +672,7 @@ __device__ __forceinline__ double tile_spmv(const PcgArgs& a, const PcgPtr& P, c
   }
   double acc[6] = {0, 0, 0, 0, 0, 0};
 #pragma unroll
-  for (int s9 = 0; s9 < 9; ++s9) {  // NormalSystem::apply (solver.cpp:80-98)
+  for (int s9 = s9_first; s9 < 9; ++s9) {  // NormalSystem::apply (solver.cpp:80-98)
     if (s9 + 1 < 9) {
       const double* bn = block(s9 + 1, vb[s9 + 1]);
 #pragma unroll
