@@ -54,3 +54,15 @@ def test_gpus_flag_spawns_ranks_with_disjoint_shards():
     assert [(r[1], r[2]) for r in ranks] == [(0, 8), (8, 16)]  # disjoint, contiguous shards
     assert ranks[0][3] != ranks[1][3]  # two processes
     assert d["max_over_ranks"] == 2.0  # the timing max reduces over both ranks
+
+
+@pytest.mark.gpu
+def test_bench_two_gpus():
+    """`bench.py --gpus 2` on a 2-GPU node: two NCCL ranks, one line with n_gpus 2 and the whole-job value. Skipped
+    on the 1-GPU boxes this project is measured on."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip(f"needs 2 GPUs, found {torch.cuda.device_count()}")
+    d = _line(["--gpus", "2", "--steps", "2", "--warmup", "3", "--batch", "8", "--no-extra", "--no-cpu"], 1200)
+    assert d["n_gpus"] == 2 and d["value"] > 0 and "x2" in d["config"]["parallelism"]
+    assert d["e2e"]["value"] > 0

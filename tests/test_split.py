@@ -207,3 +207,57 @@ def test_split_nccl_single_rank(device, mode, graph):
     p.join(timeout=60)
     assert p.exitcode == 0
     assert np.array_equal(grid, ref[0].grid_total) and np.array_equal(vis, ref[0].vis4)
+
+
+def _nccl_multi_worker(rank: int, ws: int, port: int, q, mode: str, graph: bool):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=ws)
+    try:
+        from paper_1610_07159_b200 import build
+        from paper_1610_07159_b200.hwflow import Solver
+        from paper_1610_07159_b200.split import TorchComm
+        solver = Solver(build.CUDA_LIB)
+        me = SplitRank(solver, 640, 480, DTYPE_U8, EnergyParams(), MODES_640[mode], None, rank, ws)
+        imgs = _frames(640, 480, seed=3)
+        if graph:
+            ((r, st),) = SplitGraph([me], TorchComm(me), imgs)(imgs)
+        else:
+            ((r, st),) = solve_split([me], TorchComm(me), imgs)
+        q.put((rank, r.grid_total, r.vis4, st.energy_after))
+        me.close()
+    finally:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+MODES_640 = {"schwarz": SolveSchedule(levels=4, grid_step=8, pcg_iters=5, patch_iters=5, subdomain_px=16),
+             "global": SolveSchedule(levels=4, grid_step=8, pcg_iters=5, subdomain_px=0)}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ws", [2, 4])
+@pytest.mark.parametrize("mode,graph", [("schwarz", False), ("global", False), ("global", True)])
+def test_split_nccl_multi_gpu(device, ws, mode, graph):
+    """One rank per GPU over NCCL (the halo P2P and the partial all-gathers cross devices), bitwise the unsplit
+    solve on every rank. Needs ws GPUs; skipped on the 1-GPU boxes this project is measured on."""
+    import torch
+    if torch.cuda.device_count() < ws:
+        pytest.skip(f"needs {ws} GPUs, found {torch.cuda.device_count()}")
+    imgs = _frames(640, 480, seed=3)
+    ref = _unsplit(device, imgs, MODES_640[mode])
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_nccl_multi_worker, args=(r, ws, port, q, mode, graph)) for r in range(ws)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=600) for _ in range(ws)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for _, grid, vis, ea in got:
+        assert np.array_equal(grid, ref[0].grid_total) and np.array_equal(vis, ref[0].vis4)
+        assert np.allclose(ea, ref[1].energy_after, rtol=1e-12, atol=0.0)
