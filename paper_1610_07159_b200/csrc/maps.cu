@@ -534,7 +534,20 @@ __global__ void __launch_bounds__(kReduceThreads) k_energy_reduce(const double* 
   }
 }
 
-inline dim3 rows_grid(int w, int h, int planes) { return dim3((w + kThreads - 1) / kThreads, h, planes); }
+// A row of w pixels in ceil(w / 256) CTAs of equal width (multiples of 32): 640 -> 3 x 224, 320 -> 2 x 160,
+// 160 -> 1 x 160, instead of 256-wide CTAs whose last one idles up to 7 warps.
+#ifndef HWF_ROW_ADAPT
+#define HWF_ROW_ADAPT 1
+#endif
+inline int row_threads(int w) {
+  if (!HWF_ROW_ADAPT) return kThreads;
+  const int nb = (w + kThreads - 1) / kThreads;
+  return std::max(32, ((w + nb - 1) / nb + 31) / 32 * 32);
+}
+inline dim3 rows_grid(int w, int h, int planes) {
+  const int t = row_threads(w);
+  return dim3((w + t - 1) / t, h, planes);
+}
 
 }  // namespace
 
@@ -557,10 +570,10 @@ void launch_pyr_in(const void* src, int dtype, double* dst, long long n, cudaStr
   k_pyr_in<<<static_cast<unsigned>((n + kThreads - 1) / kThreads), kThreads, 0, s>>>(src, dtype, dst, n);
 }
 void launch_pyr_down_u8(const uint8_t* src, int w, int h, double* dst, int ow, int oh, int planes, cudaStream_t s) {
-  k_pyr_down_u8<<<rows_grid(ow, oh, planes), kThreads, 0, s>>>(src, w, h, dst, ow, oh);
+  k_pyr_down_u8<<<rows_grid(ow, oh, planes), row_threads(ow), 0, s>>>(src, w, h, dst, ow, oh);
 }
 void launch_pyr_down(const double* src, int w, int h, double* dst, int ow, int oh, int planes, cudaStream_t s) {
-  k_pyr_down<<<rows_grid(ow, oh, planes), kThreads, 0, s>>>(src, w, h, dst, ow, oh);
+  k_pyr_down<<<rows_grid(ow, oh, planes), row_threads(ow), 0, s>>>(src, w, h, dst, ow, oh);
 }
 void launch_init_coarse(double* base, double* total, double* delta, int G, int B, double ox, double oy,
                         cudaStream_t s) {
@@ -570,7 +583,7 @@ void launch_init_coarse(double* base, double* total, double* delta, int G, int B
 void launch_occlusion(int w, int h, int gw, int gh, int step, const double* total, int B, int2* q, float* Z,
                       uint8_t* bad, unsigned long long* zbuf, uint8_t* degen, unsigned long long* queue,
                       unsigned int* qcount, uint8_t* vis_out, cudaStream_t s) {
-  k_occ_project<<<rows_grid(w, h, B), kThreads, 0, s>>>(w, h, gw, gh, step, total, q, Z, bad);
+  k_occ_project<<<rows_grid(w, h, B), row_threads(w), 0, s>>>(w, h, gw, gh, step, total, q, Z, bad);
   launch_occlusion_projected(w, h, B, q, Z, bad, zbuf, degen, queue, qcount, vis_out, s);
 }
 // raster + resolve from vertices already projected (by k_occ_project or the fused E_after pass)
@@ -581,21 +594,21 @@ void launch_occlusion_projected(int w, int h, int B, int2* q, float* Z, uint8_t*
   if (w >= 2 && h >= 2) {
     cudaMemsetAsync(zbuf, 0xFF, N * 4 * B * sizeof(unsigned long long), s);
     cudaMemsetAsync(qcount, 0, sizeof(unsigned int), s);
-    k_occ_raster<<<dim3((w - 1 + kThreads - 1) / kThreads, h - 1, B), kThreads, 0, s>>>(
+    k_occ_raster<<<rows_grid(w - 1, h - 1, B), row_threads(w - 1), 0, s>>>(
         w, h, q, Z, bad, zbuf, degen, queue, qcount);
     k_occ_raster_big<<<148 * 8, kThreads, 0, s>>>(w, h, q, Z, zbuf, queue, qcount);
   }
-  k_occ_resolve<<<rows_grid(w, h, B), kThreads, 0, s>>>(w, h, q, Z, bad, zbuf, degen, vis_out);
+  k_occ_resolve<<<rows_grid(w, h, B), row_threads(w), 0, s>>>(w, h, q, Z, bad, zbuf, degen, vis_out);
 }
 void launch_illumination(int w, int h, int gw, int gh, int step, const double* img, const double* total,
                          const uint8_t* vis, int B, double* resid, double* tmp, double* hm, cudaStream_t s) {
-  k_illum_resid<<<rows_grid(w, h, B), kThreads, 0, s>>>(w, h, gw, gh, step, img, total, vis, resid);
+  k_illum_resid<<<rows_grid(w, h, B), row_threads(w), 0, s>>>(w, h, gw, gh, step, img, total, vis, resid);
   if (g_gauss_r == kBlurR) {
-    k_blur_h<kBlurR><<<rows_grid(w, h, 2 * B), kThreads, 0, s>>>(w, h, resid, tmp);
-    k_blur_v_half<kBlurR><<<rows_grid(w, h, 2 * B), kThreads, 0, s>>>(w, h, tmp, hm);
+    k_blur_h<kBlurR><<<rows_grid(w, h, 2 * B), row_threads(w), 0, s>>>(w, h, resid, tmp);
+    k_blur_v_half<kBlurR><<<rows_grid(w, h, 2 * B), row_threads(w), 0, s>>>(w, h, tmp, hm);
   } else {
-    k_blur_h<-1><<<rows_grid(w, h, 2 * B), kThreads, 0, s>>>(w, h, resid, tmp);
-    k_blur_v_half<-1><<<rows_grid(w, h, 2 * B), kThreads, 0, s>>>(w, h, tmp, hm);
+    k_blur_h<-1><<<rows_grid(w, h, 2 * B), row_threads(w), 0, s>>>(w, h, resid, tmp);
+    k_blur_v_half<-1><<<rows_grid(w, h, 2 * B), row_threads(w), 0, s>>>(w, h, tmp, hm);
   }
 }
 void launch_prolong_grid(int gwc, int ghc, int gwf, int ghf, int step, const double* total_c, double* base_f,
@@ -605,7 +618,7 @@ void launch_prolong_grid(int gwc, int ghc, int gwf, int ghf, int step, const dou
 }
 void launch_prolong_maps(int wc, int hc, int wf, int hf, const uint8_t* vis_c, const double* hm_c, uint8_t* vis_f,
                          double* illum_f, int B, cudaStream_t s) {
-  k_prolong_maps<<<rows_grid(wf, hf, B), kThreads, 0, s>>>(wc, hc, wf, hf, vis_c, hm_c, vis_f, illum_f);
+  k_prolong_maps<<<rows_grid(wf, hf, B), row_threads(wf), 0, s>>>(wc, hc, wf, hf, vis_c, hm_c, vis_f, illum_f);
 }
 void launch_propagate(int gw, int gh, int step, const double* prev_delta, const double* prev_total, const double* base,
                       double* delta, double* total, int B, cudaStream_t s) {
@@ -614,7 +627,7 @@ void launch_propagate(int gw, int gh, int step, const double* prev_delta, const 
 }
 void launch_dense(int w, int h, int gw, int gh, int step, const double* total, int B, double* s_out, double* m_out,
                   double* d_out, double* disp_out, cudaStream_t s) {
-  k_dense<<<rows_grid(w, h, B), kThreads, 0, s>>>(w, h, gw, gh, step, total, s_out, m_out, d_out, disp_out);
+  k_dense<<<rows_grid(w, h, B), row_threads(w), 0, s>>>(w, h, gw, gh, step, total, s_out, m_out, d_out, disp_out);
 }
 void launch_energy_reduce(const double* ep, int nslots, int cap, int B, double* out, int* flags, cudaStream_t s) {
   k_energy_reduce<<<static_cast<unsigned>(nslots * B), kReduceThreads, 0, s>>>(ep, nslots, cap, B, out, flags);
