@@ -154,7 +154,11 @@ __device__ __forceinline__ void raster_row_tests(const Tri& T, int yy, int x0, i
     bool in = true;
 #pragma unroll
     for (int i = 0; i < 3; ++i) in = in && (R.E[i] > 0 || (R.E[i] == 0 && R.tl[i]));
+#ifdef HWF_DIAG_RASTER_NO_ATOMIC  // diagnostic A/B only (wrong results): coverage without the z-buffer atomics
+    if (in && key == 0) row[xx] = key;
+#else
     if (in) atomicMin(row + xx, key);
+#endif
 #pragma unroll
     for (int i = 0; i < 3; ++i) R.E[i] += R.step[i];
   }
