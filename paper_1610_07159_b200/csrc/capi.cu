@@ -404,6 +404,18 @@ int hwf_set_profiling(hwf_ctx* ctx, int on) {
   return HWF_OK;
 }
 int hwf_launch_count(hwf_ctx* ctx) { return ctx && ctx->plan ? ctx->plan->launches : 0; }
+int hwf_gn_iteration_times(hwf_ctx* ctx, int cap, double* ms, int* level) {
+  if (!ctx || !ctx->plan || !ctx->plan->profile) return -1;
+  Plan& p = *ctx->plan;
+  const int n = static_cast<int>(p.gev_level.size());
+  for (int i = 0; i < n && i < cap; ++i) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, p.gev[2 * i], p.gev[2 * i + 1]) != cudaSuccess) return -1;
+    ms[i] = t;
+    level[i] = p.gev_level[i];
+  }
+  return n;
+}
 int hwf_pixel_kernel_times(hwf_ctx* ctx, int cap, double* ms, double* bytes) {
   if (!ctx || !ctx->plan || !ctx->plan->profile) return -1;
   Plan& p = *ctx->plan;

@@ -174,6 +174,9 @@ struct Launches {
   int count = 0;
   std::vector<cudaEvent_t>* ev = nullptr;  // pixel-kernel timing events (optional)
   std::vector<double>* bytes = nullptr;
+  std::vector<cudaEvent_t>* gn_ev = nullptr;  // per-GN-iteration timing events (optional): 2 per iteration
+  std::vector<int>* gn_level = nullptr;       // the level of each timed iteration
+  int level = 0;                              // the level record_gn_level is recording
 };
 
 // Algorithmic bytes of one k_pixel<LIN> launch: every
@@ -306,6 +309,8 @@ inline void record_gn_level(LevelDev& d, int B, const hwf_energy_params& P, cons
                             Launches& L, const uint8_t* src8 = nullptr, bool energy_after = true,
                             double* pcg_trace = nullptr) {  // device [gn][pcg_iters + 1], global mode, B = 1
   for (int it = 0; it < gn; ++it) {
+    const size_t gi = L.gn_level ? L.gn_level->size() : 0;
+    if (L.gn_ev) CK(cudaEventRecordWithFlags((*L.gn_ev)[2 * gi], st, cudaEventRecordExternal));
     rec_linearize(d, B, P, S, dF, it, E, slot_base, flags, st, L, src8);
     if (S.subdomain_px > 0) {
       for (int s = 0; s < S.patch_iters; ++s) rec_sweep(d, B, S, s, flags, st, L);
@@ -318,6 +323,10 @@ inline void record_gn_level(LevelDev& d, int B, const hwf_energy_params& P, cons
       ga.delta = d.delta; ga.total = d.total; ga.base = d.base; ga.active = S.active_fields; ga.flags = flags;
       launch_pcg_global(ga, B, st);
       L.count += pcg_launches(d.gw, d.gh, S.pcg_iters);
+    }
+    if (L.gn_ev) {  // linearisation + solve of one GN iteration (the E_after pass of a level's last is not in it)
+      CK(cudaEventRecordWithFlags((*L.gn_ev)[2 * gi + 1], st, cudaEventRecordExternal));
+      L.gn_level->push_back(L.level);
     }
   }
   if (gn > 0 && energy_after) rec_energy_after(d, B, P, S, dF, gn, E, slot_base, flags, st, L, src8);
@@ -365,6 +374,8 @@ struct Plan {
   int launches = 0;
   std::vector<cudaEvent_t> ev;
   std::vector<double> ev_bytes;
+  std::vector<cudaEvent_t> gev;  // profile: two events per GN iteration
+  std::vector<int> gev_level;
 
   bool matches(int B_, int w_, int h_, int dt, const hwf_energy_params& P_, const hwf_schedule& S_, const double* F_,
                unsigned om, bool prof, bool prev) const {
@@ -380,6 +391,7 @@ struct Plan {
     if (exec_slot[1]) cudaGraphExecDestroy(exec_slot[1]);
     if (graph2) cudaGraphDestroy(graph2);
     for (auto e : ev) cudaEventDestroy(e);
+    for (auto e : gev) cudaEventDestroy(e);
     for (int k = 0; k < 2; ++k) {
       if (h_red[k]) cudaFreeHost(h_red[k]);
       if (h_flags[k]) cudaFreeHost(h_flags[k]);
@@ -514,6 +526,8 @@ struct Plan {
       for (int l = 0; l < L; ++l) total_gn += gn[l];
       ev.resize(2 * std::max(total_gn, 1));
       for (auto& e : ev) CK(cudaEventCreate(&e));
+      gev.resize(2 * std::max(total_gn, 1));
+      for (auto& e : gev) CK(cudaEventCreate(&e));
     }
   }
 
@@ -522,13 +536,17 @@ struct Plan {
   void record(cudaStream_t st) {
     Launches LC;
     ev_bytes.clear();
+    gev_level.clear();
     if (profile) {
       LC.ev = &ev;
       LC.bytes = &ev_bytes;
+      LC.gn_ev = &gev;
+      LC.gn_level = &gev_level;
     }
     rec_prologue(st, LC);
     for (int l = L - 1; l >= 0; --l) {
       rec_level_begin(l, st, LC);
+      LC.level = l;
       record_gn_level(lv[l], B, P, S, dF, gn[l], E, slot_base[l], sc, flags, st, LC, src8(l), false);
       if (gn[l] > 0) {
         // E_after of the level's last iteration (stats) fused with the occlusion projection of the same flow:

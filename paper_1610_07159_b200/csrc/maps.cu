@@ -415,6 +415,73 @@ __global__ void k_blur_v_half(int w, int h, const double* __restrict__ src, doub
   dst[static_cast<size_t>(plane) * w * h + static_cast<size_t>(y) * w + x] = 0.5 * acc;  // +-blur/2 split
 }
 
+// The pinned radius, K outputs per thread from a register window of K + 2R inputs (the same FMA sequence per
+// output as k_blur_h / k_blur_v_half, so the same doubles), instead of 2R + 1 loads per output.
+// Horizontal: a warp stages a row segment of 32 K outputs plus the 2R halo in shared memory (one pad double per
+// K, so the lanes' K-strided window reads are conflict-free), warps over flattened (row, segment) items;
+// 160-wide segments fit the 320 / 160 px levels exactly. Vertical: a thread walks kBlurK rows of its column,
+// loads coalesced across the warp.
+constexpr int kBlurK = 8, kBlurHK = 5, kBlurWarps = 4;  // vertical / horizontal outputs per thread
+template <int R>
+__global__ void __launch_bounds__(32 * kBlurWarps) k_blur_h_win(int w, int h, int segs, int items,
+                                                                const double* __restrict__ src,
+                                                                double* __restrict__ dst) {
+  constexpr int K = kBlurHK, kSpan = 32 * K + 2 * R, kPitch = kSpan + kSpan / K + 1;
+  __shared__ double sm[kBlurWarps][kPitch];
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5, plane = blockIdx.y;
+  const int item = blockIdx.x * kBlurWarps + wi;  // (row, segment of 32 K outputs) of this warp
+  if (item >= items) return;  // the whole warp
+  const int y = item / segs, seg0 = (item - y * segs) * 32 * K;
+  const double* S = src + static_cast<size_t>(plane) * w * h + static_cast<size_t>(y) * w;
+  for (int j = lane; j < kSpan; j += 32) sm[wi][j + j / K] = __ldg(S + min(max(seg0 - R + j, 0), w - 1));
+  __syncwarp();
+  double v[K + 2 * R];
+#pragma unroll
+  for (int t = 0; t < K + 2 * R; ++t) {
+    const int j = lane * K + t;
+    v[t] = sm[wi][j + j / K];
+  }
+  double o[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double acc = 0.0;
+#pragma unroll
+    for (int i = -R; i <= R; ++i) acc += c_gauss[i + R] * v[k + i + R];
+    o[k] = acc;
+  }
+  // through the same shared row, so the stores are coalesced
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int j = lane * K + k;
+    sm[wi][j + j / K] = o[k];
+  }
+  __syncwarp();
+  double* D = dst + static_cast<size_t>(plane) * w * h + static_cast<size_t>(y) * w;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int j = k * 32 + lane, x = seg0 + j;
+    if (x < w) D[x] = sm[wi][j + j / K];
+  }
+}
+template <int R>
+__global__ void k_blur_v_half_win(int w, int h, const double* __restrict__ src, double* __restrict__ dst) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y0 = blockIdx.y * kBlurK, plane = blockIdx.z;
+  if (x >= w) return;
+  const double* S = src + static_cast<size_t>(plane) * w * h + x;
+  double v[kBlurK + 2 * R];
+#pragma unroll
+  for (int t = 0; t < kBlurK + 2 * R; ++t) v[t] = __ldg(S + static_cast<size_t>(min(max(y0 - R + t, 0), h - 1)) * w);
+  double* D = dst + static_cast<size_t>(plane) * w * h + x;
+#pragma unroll
+  for (int k = 0; k < kBlurK; ++k) {
+    double acc = 0.0;
+#pragma unroll
+    for (int i = -R; i <= R; ++i) acc += c_gauss[i + R] * v[k + i + R];
+    if (y0 + k < h) D[static_cast<size_t>(y0 + k) * w] = 0.5 * acc;  // +-blur/2 split
+  }
+}
+
 // ---- prolongation (pins C.1/C.3/C.4) ---------------------
 __global__ void k_prolong_grid(int gwc, int ghc, int gwf, int ghf, int step, const double* __restrict__ tc,
                                double* __restrict__ base, double* __restrict__ total, double* __restrict__ delta) {
@@ -443,13 +510,27 @@ __global__ void k_prolong_maps(int wc, int hc, int wf, int hf, const uint8_t* __
   const size_t Nc = static_cast<size_t>(wc) * hc, Nf = static_cast<size_t>(wf) * hf;
   const size_t pix = static_cast<size_t>(y) * wf + x;
   const uint8_t* V = vc + pair * Nc;
-  const Coord cx = cell_coord(x / 2.0, wc), cy = cell_coord(y / 2.0, hc);
-  const int x1 = min(cx.i0 + 1, wc - 1), y1 = min(cy.i0 + 1, hc - 1);
-  const uint8_t q00 = V[static_cast<size_t>(cy.i0) * wc + cx.i0], q10 = V[static_cast<size_t>(cy.i0) * wc + x1];
-  const uint8_t q01 = V[static_cast<size_t>(y1) * wc + cx.i0], q11 = V[static_cast<size_t>(y1) * wc + x1];
-  // x / 2 leaves fractions in {0, 1/2, 1}, so the bilinear weights are quarters and the test
-  // sum >= 0.5 is exact in integers: 4 * sum >= 2 (pin C.3)
-  const int fx2 = static_cast<int>(cx.f * 2.0), fy2 = static_cast<int>(cy.f * 2.0);
+  // cell_coord(x / 2, wc) (image.cpp:19-31) in integers: x / 2 leaves fractions in {0, 1/2, 1}, so with
+  // f2 = 2 f the bilinear weights are quarters and the test sum >= 0.5 is exact: 4 * sum >= 2 (pin C.3)
+  auto half_coord = [](int v, int n, int& i0, int& f2) {
+    if (n == 1 || v == 0) {  // v / 2 <= 0 (or a single column): cell 0, f = 0
+      i0 = 0;
+      f2 = 0;
+    } else if (v >= 2 * (n - 1)) {  // v / 2 >= n - 1: cell n - 2, f = 1
+      i0 = n - 2;
+      f2 = 2;
+    } else {
+      i0 = v >> 1;
+      f2 = v & 1;
+    }
+  };
+  int cx0, fx2, cy0, fy2;
+  half_coord(x, wc, cx0, fx2);
+  half_coord(y, hc, cy0, fy2);
+  const int x1 = min(cx0 + 1, wc - 1), y1 = min(cy0 + 1, hc - 1);
+  const uint8_t* R0 = V + cy0 * wc;
+  const uint8_t* R1 = V + y1 * wc;
+  const uint8_t q00 = R0[cx0], q10 = R0[x1], q01 = R1[cx0], q11 = R1[x1];
   const int w00 = (2 - fx2) * (2 - fy2), w10 = fx2 * (2 - fy2), w01 = (2 - fx2) * fy2, w11 = fx2 * fy2;
   uint8_t bits = 0;
 #pragma unroll
@@ -608,8 +689,16 @@ void launch_illumination(int w, int h, int gw, int gh, int step, const double* i
                          const uint8_t* vis, int B, double* resid, double* tmp, double* hm, cudaStream_t s) {
   k_illum_resid<<<rows_grid(w, h, B), row_threads(w), 0, s>>>(w, h, gw, gh, step, img, total, vis, resid);
   if (g_gauss_r == kBlurR) {
+#ifdef HWF_BLUR_PER_TAP  // A/B: one output per thread, 2R + 1 loads each
     k_blur_h<kBlurR><<<rows_grid(w, h, 2 * B), row_threads(w), 0, s>>>(w, h, resid, tmp);
     k_blur_v_half<kBlurR><<<rows_grid(w, h, 2 * B), row_threads(w), 0, s>>>(w, h, tmp, hm);
+#else
+    const int segs = (w + 32 * kBlurHK - 1) / (32 * kBlurHK), items = segs * h;
+    k_blur_h_win<kBlurR><<<dim3((items + kBlurWarps - 1) / kBlurWarps, 2 * B), 32 * kBlurWarps, 0, s>>>(
+        w, h, segs, items, resid, tmp);
+    k_blur_v_half_win<kBlurR><<<dim3((w + row_threads(w) - 1) / row_threads(w), (h + kBlurK - 1) / kBlurK, 2 * B),
+                                row_threads(w), 0, s>>>(w, h, tmp, hm);
+#endif
   } else {
     k_blur_h<-1><<<rows_grid(w, h, 2 * B), row_threads(w), 0, s>>>(w, h, resid, tmp);
     k_blur_v_half<-1><<<rows_grid(w, h, 2 * B), row_threads(w), 0, s>>>(w, h, tmp, hm);
