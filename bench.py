@@ -439,6 +439,14 @@ def run_ours(args, ws, rank, local):
         prof = json.loads(tf.read_text())
         v = prof.get("dram_bytes_per_launch_L0")
         traffic = v * B / prof.get("batch", 128) if v is not None else None
+    # per Gauss-Newton iteration (linearisation + PCG) of the last timed replay, CUDA events inside the graph
+    gms, glv = (C.c_double * cap)(), (C.c_int * cap)()
+    ng = lib.hwf_gn_iteration_times(h, cap, gms, glv)
+    gn_iter = {}
+    for i in range(max(ng, 0)):
+        gn_iter.setdefault(f"L{glv[i]}", []).append(gms[i])
+    gn_iter = {k: {"iters": len(v), "batch_ms": sum(v) / len(v), "per_pair_us": 1000.0 * sum(v) / len(v) / B}
+               for k, v in sorted(gn_iter.items())}
     launches = lib.hwf_launch_count(h)
     # FP64 roofline of the same kernel: FP64 flops per launch from the committed ncu capture (scaled by the batch),
     # over this run's CUDA-event launch time, against the builder-measured DFMA peak (profiles/fp64_peak.json)
@@ -483,7 +491,8 @@ def run_ours(args, ws, rank, local):
             "config": {"workload": workload_desc(args.mode), "pairs_per_gpu_per_step": B,
                        "global_pairs_per_step": ws * B, "parallelism": f"frame-sharded x{ws} (no collective)",
                        "l2": "no flush: per-step working set > 3 GB >> 126 MB L2"},
-            "ms_per_gn_iter": ms_per_step / gn_total / B,
+            "ms_per_gn_iter": ms_per_step / gn_total / B,  # whole step per pair per GN iteration (amortised)
+            "gn_iter_by_level": gn_iter,  # measured: one GN iteration (linearise + solve) of the B-pair batch
             "hbm_gbs": achieved,  # dominant kernel, algorithmic bytes / CUDA-event time
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"] if pk["hbm_gbs"] else None, "traffic": traffic,

@@ -27,12 +27,15 @@ int hwf_run_device(hwf_ctx* ctx);
 int hwf_sync(hwf_ctx* ctx, hwf_stats* stats);
 /* cudaStream_t of the context (for events / external stream wrapping). */
 void* hwf_stream(hwf_ctx* ctx);
-/* When on, plans built afterwards record CUDA events around every k_pixel<LIN> launch. */
+/* When on, plans built afterwards record CUDA events around every k_pixel<LIN> launch and every GN iteration. */
 int hwf_set_profiling(hwf_ctx* ctx, int on);
 /* Kernel launches in one replay of the current plan. */
 int hwf_launch_count(hwf_ctx* ctx);
 /* Per-launch duration (ms) and algorithmic bytes of k_pixel<LIN> from the last replay. */
 int hwf_pixel_kernel_times(hwf_ctx* ctx, int cap, double* ms, double* bytes);
+/* Per Gauss-Newton iteration of the last replay (profiling plans): duration (ms) of its linearisation and
+ * solve, and its level (0 = finest). Returns the count, or -1 without a profiling plan. */
+int hwf_gn_iteration_times(hwf_ctx* ctx, int cap, double* ms, int* level);
 
 /* Streaming: enqueue one batch from host memory and return immediately; batch k's
  * upload and batch k-1's download overlap batch k's device solve (two slots, at

@@ -150,6 +150,7 @@ _EXT_SIGS = {
     "hwf_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
     "hwf_launch_count": (C.c_int, [C.c_void_p]),
     "hwf_pixel_kernel_times": (C.c_int, [C.c_void_p, C.c_int, _dp, _dp]),
+    "hwf_gn_iteration_times": (C.c_int, [C.c_void_p, C.c_int, _dp, C.POINTER(C.c_int)]),
     "hwf_submit_batch": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(Frame4C), C.POINTER(EnergyParamsC),
                                    C.POINTER(ScheduleC), _dp, C.POINTER(ResultC), C.POINTER(StatsC)]),
     "hwf_wait": (C.c_int, [C.c_void_p]),

@@ -35,15 +35,26 @@ __global__ void k_pyr_down_u8(const uint8_t* __restrict__ src, int w, int h, dou
   const int plane = blockIdx.z;
   if (x >= ow) return;
   const uint8_t* S = src + static_cast<size_t>(plane) * w * h;
+  // k/255 correctly rounded as fma(k, hi, k * lo), exhaustively checked (pixel.cu u8val)
+  auto u8v = [](int k8) {
+    const double k = static_cast<double>(k8);
+    return __fma_rn(k, 1.0 / 255.0, __dmul_rn(k, 5.4633625097902372e-20));
+  };
+  if (2 * x + 1 < w && 2 * y + 1 < h) {  // all four taps, in the loop's order (0,0), (1,0), (0,1), (1,1)
+    const uint8_t* r0 = S + static_cast<size_t>(2 * y) * w + 2 * x;
+    const uint8_t* r1 = r0 + w;
+    const int a = r0[0], b = r0[1], c = r1[0], d = r1[1];
+    dst[static_cast<size_t>(plane) * ow * oh + static_cast<size_t>(y) * ow + x] =
+        __dmul_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(0.0, u8v(a)), u8v(b)), u8v(c)), u8v(d)), 0.25);
+    return;
+  }
   double sum = 0.0;
   int cnt = 0;
   for (int dy = 0; dy < 2; ++dy)
     for (int dx = 0; dx < 2; ++dx) {
       const int sx = 2 * x + dx, sy = 2 * y + dy;
       if (sx < w && sy < h) {
-        // k/255 correctly rounded as fma(k, hi, k * lo), exhaustively checked (pixel.cu u8val)
-        const double k = static_cast<double>(S[static_cast<size_t>(sy) * w + sx]);
-        sum = __dadd_rn(sum, __fma_rn(k, 1.0 / 255.0, __dmul_rn(k, 5.4633625097902372e-20)));
+        sum = __dadd_rn(sum, u8v(S[static_cast<size_t>(sy) * w + sx]));
         ++cnt;
       }
     }
@@ -58,6 +69,14 @@ __global__ void k_pyr_down(const double* __restrict__ src, int w, int h, double*
   const int plane = blockIdx.z;
   if (x >= ow) return;
   const double* S = src + static_cast<size_t>(plane) * w * h;
+  if (2 * x + 1 < w && 2 * y + 1 < h) {  // all four taps, in the loop's order
+    const double* r0 = S + static_cast<size_t>(2 * y) * w + 2 * x;
+    const double* r1 = r0 + w;
+    const double a = r0[0], b = r0[1], c = r1[0], d = r1[1];
+    dst[static_cast<size_t>(plane) * ow * oh + static_cast<size_t>(y) * ow + x] =
+        __dmul_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(0.0, a), b), c), d), 0.25);
+    return;
+  }
   double sum = 0.0;
   int cnt = 0;
   for (int dy = 0; dy < 2; ++dy)
@@ -549,6 +568,62 @@ __global__ void k_prolong_maps(int wc, int hc, int wf, int hf, const uint8_t* __
   }
 }
 
+// The masks alone (the pipeline: illumination is read from the coarse half maps by k_pixel), kProlongPx fine
+// pixels of a row per thread: the row's coarse coordinates and byte rows are shared, one 32-bit store when the
+// row allows it. Same integer arithmetic as k_prolong_maps.
+constexpr int kProlongPx = 4;
+__global__ void k_prolong_vis(int wc, int hc, int wf, int hf, const uint8_t* __restrict__ vc, uint8_t* __restrict__ vf) {
+  const int x4 = kProlongPx * (blockIdx.x * blockDim.x + threadIdx.x), y = blockIdx.y, pair = blockIdx.z;
+  if (x4 >= wf) return;
+  const size_t Nc = static_cast<size_t>(wc) * hc, Nf = static_cast<size_t>(wf) * hf;
+  int cy0, fy2;
+  if (hc == 1 || y == 0) {
+    cy0 = 0;
+    fy2 = 0;
+  } else if (y >= 2 * (hc - 1)) {
+    cy0 = hc - 2;
+    fy2 = 2;
+  } else {
+    cy0 = y >> 1;
+    fy2 = y & 1;
+  }
+  const int y1 = min(cy0 + 1, hc - 1);
+  const uint8_t* R0 = vc + pair * Nc + cy0 * wc;
+  const uint8_t* R1 = vc + pair * Nc + y1 * wc;
+  uint32_t packed = 0;
+#pragma unroll
+  for (int k = 0; k < kProlongPx; ++k) {
+    const int x = x4 + k;
+    int cx0, fx2;
+    if (wc == 1 || x == 0) {
+      cx0 = 0;
+      fx2 = 0;
+    } else if (x >= 2 * (wc - 1)) {
+      cx0 = wc - 2;
+      fx2 = 2;
+    } else {
+      cx0 = x >> 1;
+      fx2 = x & 1;
+    }
+    const int x1 = min(cx0 + 1, wc - 1);
+    const int q00 = R0[cx0], q10 = R0[x1], q01 = R1[cx0], q11 = R1[x1];
+    const int w00 = (2 - fx2) * (2 - fy2), w10 = fx2 * (2 - fy2), w01 = (2 - fx2) * fy2, w11 = fx2 * fy2;
+    uint32_t bits = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int v4 = w00 * ((q00 >> e) & 1) + w10 * ((q10 >> e) & 1) + w01 * ((q01 >> e) & 1) + w11 * ((q11 >> e) & 1);
+      bits |= v4 >= 2 ? (1u << e) : 0u;
+    }
+    packed |= bits << (8 * k);
+  }
+  uint8_t* out = vf + pair * Nf + static_cast<size_t>(y) * wf + x4;
+  if (x4 + kProlongPx <= wf && (reinterpret_cast<uintptr_t>(out) & 3) == 0) {
+    *reinterpret_cast<uint32_t*>(out) = packed;
+  } else {
+    for (int k = 0; k < kProlongPx && x4 + k < wf; ++k) out[k] = static_cast<uint8_t>(packed >> (8 * k));
+  }
+}
+
 // ---- temporal propagation (pin in oracle/hierarchy.cpp) ---
 // next_delta(p) = prev_delta(p - 2 m_prev(p)) (exact bilinear, zero outside the
 // lattice); total = base + delta.
@@ -711,6 +786,11 @@ void launch_prolong_grid(int gwc, int ghc, int gwf, int ghf, int step, const dou
 }
 void launch_prolong_maps(int wc, int hc, int wf, int hf, const uint8_t* vis_c, const double* hm_c, uint8_t* vis_f,
                          double* illum_f, int B, cudaStream_t s) {
+  if (!hm_c || !illum_f) {  // masks only (the pipeline)
+    const int n4 = (wf + kProlongPx - 1) / kProlongPx;
+    k_prolong_vis<<<rows_grid(n4, hf, B), row_threads(n4), 0, s>>>(wc, hc, wf, hf, vis_c, vis_f);
+    return;
+  }
   k_prolong_maps<<<rows_grid(wf, hf, B), row_threads(wf), 0, s>>>(wc, hc, wf, hf, vis_c, hm_c, vis_f, illum_f);
 }
 void launch_propagate(int gw, int gh, int step, const double* prev_delta, const double* prev_total, const double* base,
