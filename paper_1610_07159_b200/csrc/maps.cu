@@ -606,15 +606,20 @@ __global__ void k_prolong_vis(int wc, int hc, int wf, int hf, const uint8_t* __r
       fx2 = x & 1;
     }
     const int x1 = min(cx0 + 1, wc - 1);
-    const int q00 = R0[cx0], q10 = R0[x1], q01 = R1[cx0], q11 = R1[x1];
-    const int w00 = (2 - fx2) * (2 - fy2), w10 = fx2 * (2 - fy2), w01 = (2 - fx2) * fy2, w11 = fx2 * fy2;
-    uint32_t bits = 0;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int v4 = w00 * ((q00 >> e) & 1) + w10 * ((q10 >> e) & 1) + w01 * ((q01 >> e) & 1) + w11 * ((q11 >> e) & 1);
-      bits |= v4 >= 2 ? (1u << e) : 0u;
+    const uint32_t q00 = R0[cx0], q10 = R0[x1], q01 = R1[cx0], q11 = R1[x1];
+    // the quarter weights (2 - fx2, fx2) x (2 - fy2, fy2) make "4 * sum >= 2" a bitwise vote over the four masks:
+    // one corner of weight 4 (fx2, fy2 even), two of weight 2 (either one), or four of weight 1 (at least two)
+    uint32_t bits;
+    if (fx2 == 1 && fy2 == 1) {
+      bits = (q00 & q10) | (q01 & q11) | ((q00 | q10) & (q01 | q11));
+    } else if (fx2 == 1) {
+      bits = fy2 == 2 ? (q01 | q11) : (q00 | q10);
+    } else if (fy2 == 1) {
+      bits = fx2 == 2 ? (q10 | q11) : (q00 | q01);
+    } else {
+      bits = fx2 == 2 ? (fy2 == 2 ? q11 : q10) : (fy2 == 2 ? q01 : q00);
     }
-    packed |= bits << (8 * k);
+    packed |= (bits & 0xFu) << (8 * k);
   }
   uint8_t* out = vf + pair * Nf + static_cast<size_t>(y) * wf + x4;
   if (x4 + kProlongPx <= wf && (reinterpret_cast<uintptr_t>(out) & 3) == 0) {
