@@ -169,11 +169,10 @@ __device__ __forceinline__ void raster_row_tests(const Tri& T, int yy, int x0, i
     R.tl[i] = dy > 0 || (dy == 0 && dx < 0);
   }
   unsigned long long* row = zb + static_cast<size_t>(yy) * w;
-  // E > 0, or E == 0 on a top-left edge, is E + tl > 0 for an integer E: one min over the three biased edges
-#pragma unroll
-  for (int i = 0; i < 3; ++i) R.E[i] += R.tl[i] ? 1 : 0;
   for (int xx = x0; xx <= x1; ++xx) {
-    const bool in = min(R.E[0], min(R.E[1], R.E[2])) > 0;
+    bool in = true;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) in = in && (R.E[i] > 0 || (R.E[i] == 0 && R.tl[i]));
 #ifdef HWF_DIAG_RASTER_NO_ATOMIC  // diagnostic A/B only (wrong results): coverage without the z-buffer atomics
     if (in && key == 0) row[xx] = key;
 #else
@@ -236,38 +235,7 @@ __device__ __forceinline__ bool raster_tri(int w, int h, const Tri& T, bool any_
     return false;
   }
   const unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(zf)) << 32) | tri;
-#ifdef HWF_RASTER_ROW_SETUP  // A/B: the edge functions set up again for every row
   for (int yy = y0; yy <= y1; ++yy) raster_row_tests(T, yy, x0, x1, w, zb, key);
-#else
-  // the three edge functions at the box's first pixel centre, biased by the top-left rule (E + tl > 0), then
-  // stepped by -256 dy per column and +256 dx per row (exact int32 inside the <= 8 px box, as above)
-  int E[3], sx[3], sy[3];
-  const int Px0 = x0 * 256, Py0 = y0 * 256;
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    const int j = (i + 1) % 3;
-    const int dx = T.X[j] - T.X[i], dy = T.Y[j] - T.Y[i];
-    E[i] = dx * (Py0 - T.Y[i]) - dy * (Px0 - T.X[i]) + ((dy > 0 || (dy == 0 && dx < 0)) ? 1 : 0);
-    sx[i] = -256 * dy;
-    sy[i] = 256 * dx;
-  }
-  unsigned long long* row = zb + static_cast<size_t>(y0) * w;
-  for (int yy = y0; yy <= y1; ++yy, row += w) {
-    int e0 = E[0], e1 = E[1], e2 = E[2];
-    for (int xx = x0; xx <= x1; ++xx) {
-#ifdef HWF_DIAG_RASTER_NO_ATOMIC  // diagnostic A/B only (wrong results): coverage without the z-buffer atomics
-      if (min(e0, min(e1, e2)) > 0 && key == 0) row[xx] = key;
-#else
-      if (min(e0, min(e1, e2)) > 0) atomicMin(row + xx, key);
-#endif
-      e0 += sx[0];
-      e1 += sx[1];
-      e2 += sx[2];
-    }
-#pragma unroll
-    for (int i = 0; i < 3; ++i) E[i] += sy[i];
-  }
-#endif
   return false;
 }
 
