@@ -130,3 +130,22 @@ def test_c_abi_nulls_and_limits(device):
     assert lib.hwf_solve_pair(h, C.byref(fr), C.byref(P), C.byref(S_max), None, C.byref(out), C.byref(st)) in (
         capi.HWF_OK, capi.HWF_EDIVERGED)
     assert st.levels_used >= 1 and st.gn_iters[0] == 32
+
+
+@pytest.mark.parametrize("step,w,h", [(16, 120, 88), (32, 200, 136), (12, 97, 61)])
+def test_linearize_large_and_odd_steps_match_oracle(device, oracle, step, w, h):
+    """hwf_linearize at grid steps >= 16 (k_pixel's 14-double operand-pair records instead of the 27 products: a tile
+    is one cell of up to 33 x 33 pixels) and at a non-power-of-two step (the correctly rounded x / step), through
+    the thread-per-node assembly: blocks, rhs and preconditioner against the oracle."""
+    rng = np.random.default_rng(step)
+    imgs = synthetic.render_pair(w, h, s=(1.2, 0.2), m=(0.5, -0.4), seed=step, dtype=np.float64)
+    gw, gh = grid_dims(w, h, step)
+    lv = LevelState(imgs, step, rng.normal(0, 0.6, (gw * gh, 6)), rng.normal(0, 0.2, (gw * gh, 6)),
+                    rng.integers(0, 16, (h, w)).astype(np.uint8), (rng.random((h, w)) > 0.1).astype(np.uint8),
+                    rng.uniform(1, 100, gw * gh), rng.normal(0, 0.02, (4, h, w)),
+                    np.array([[0, 0, 0], [0, 0, -1], [0, 1, 0.0]]))  # rectified rig (the facial preset's epipolar term)
+    for preset in ("live", "facial"):
+        P = EnergyParams.preset(preset)
+        a, b = device.build_normal_system(lv, P), oracle.build_normal_system(lv, P)
+        for x, y in zip(a, b):
+            np.testing.assert_allclose(x, y, rtol=STAGE_RTOL, atol=STAGE_RTOL * np.abs(y).max())
