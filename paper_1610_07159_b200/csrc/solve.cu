@@ -846,10 +846,163 @@ __global__ void __launch_bounds__(kPcgThreads) k_pcg_scalars(const PcgArgs a, in
   }
 }
 
+// Small levels (every tile of a pair fits one CTA: <= 16 tiles): the whole pcg_solve of a pair in ONE CTA, a
+// warp per tile exactly as the per-phase kernels map them, so every per-node value, every tile partial (warp xor
+// tree) and every pair total (pair_total's order over the partials, here in shared memory) is the same double as
+// theirs; the phases meet at __syncthreads instead of kernel boundaries and last-CTA atomics (11 launches per GN
+// iteration at these levels were latency, not work). x, r, z, Ap and the preconditioner stay in registers; p lives
+// in shared memory, where the 9-slot SpMV reads the neighbours' values; the system is read from global (L2).
+constexpr int kFusedMaxTiles = 16;  // 512 threads: 128 registers, no spills
+__device__ __forceinline__ double pair_total_smem(const double* part, int n, int stride, double* red) {
+  // pair_total's summation order (128-thread stride, xor trees, the 4 warps in order) over shared memory
+  double s = 0.0;
+  if (threadIdx.x < kPcgThreads)
+    for (int k = threadIdx.x; k < n; k += kPcgThreads) s += part[k * stride];
+  s = warp_sum(s);
+  __syncthreads();
+  if (threadIdx.x < kPcgThreads && (threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int w = 0; w < kPcgWarps; ++w) t += red[w];
+  __syncthreads();  // red and part reusable
+  return t;
+}
+
+__global__ void __launch_bounds__(32 * kFusedMaxTiles) k_pcg_fused(const PcgArgs a) {
+  extern __shared__ __align__(16) double fsm[];
+  const int pair = blockIdx.x, tile = threadIdx.x >> 5, j = threadIdx.x & 31;
+  const PcgPtr P = pcg_ptr(a, pair);
+  double* ps = fsm;                         // p, node-major [G][6]
+  double* part = fsm + 6 * P.G;             // [ntiles][2]
+  double* red = part + 2 * kFusedMaxTiles;  // [kPcgWarps]
+  const PcgTile T = pcg_tile_at(a.gw, a.gh, tile, P.ntiles);
+  const bool act = j < T.width;
+  const int a_ = T.a0 + min(j, max(T.width - 1, 0));
+  const size_t n = static_cast<size_t>(T.b) * a.gw + a_;
+  const bool want_rr = P.tr != nullptr;
+  // k_pcg_init
+  double r[6], z[6], x[6] = {0, 0, 0, 0, 0, 0};
+#pragma unroll
+  for (int k = 0; k < 6; ++k) r[k] = act ? __ldg(P.sys + (kSysRhs + k) * P.G + n) : 0.0;
+  pcg_precond(P, n, r, z);  // (the preconditioner is re-read per update: L2 hits, fewer live registers)
+  for (int i = threadIdx.x; i < 6 * static_cast<int>(P.G); i += blockDim.x) ps[i] = 0.0;  // p_prev = 0
+  {
+    const double prz = tile_partial(act, node_dot(r, z)), prr = tile_partial(act, node_dot(r, r));
+    if (j == 0 && T.live) {
+      part[2 * tile] = prz;
+      part[2 * tile + 1] = prr;
+    }
+  }
+  __syncthreads();
+  double rz = pair_total_smem(part, P.ntiles, 2, red);
+  const double rr0 = pair_total_smem(part + 1, P.ntiles, 2, red);
+  const double rz0 = fabs(rz);
+  double beta = 0.0, alpha = 0.0;
+  bool stop = rz == 0.0;  // solver.cpp:334-338
+  if (threadIdx.x == 0 && P.tr) {
+    P.tr[0] = sqrt(rr0);
+    if (stop)
+      for (int it = 0; it < a.iters; ++it) P.tr[it + 1] = 0.0;
+  }
+  for (int it = 0; it < a.iters && !stop; ++it) {
+    // k_pcg_spmv: p = z + beta p (solver.cpp:358), then Ap over the 9 slots in the per-phase kernel's order
+    double pown[6];
+    if (act) {
+#pragma unroll
+      for (int c = 0; c < 6; ++c) pown[c] = z[c] + beta * ps[6 * n + c];
+    }
+    __syncthreads();  // every neighbour has read the previous p
+    if (act) {
+#pragma unroll
+      for (int c = 0; c < 6; ++c) ps[6 * n + c] = pown[c];
+    }
+    __syncthreads();
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+#pragma unroll 1
+    for (int s9 = 0; s9 < 9; ++s9) {  // NormalSystem::apply (solver.cpp:80-98)
+      const int dx = s9 % 3 - 1, dy = s9 / 3 - 1;
+      const int qa = a_ + dx, qb = T.b + dy;
+      if (!(act && qa >= 0 && qa < a.gw && qb >= 0 && qb < a.gh)) continue;
+      const size_t nq = static_cast<size_t>(qb) * a.gw + qa;
+      const double* blk = P.sys + static_cast<size_t>(s9 >= 4 ? s9 - 4 : 4 - s9) * 21 * P.G + (s9 >= 4 ? n : nq);
+      double A[21];
+#pragma unroll
+      for (int m = 0; m < 21; ++m) A[m] = __ldg(blk + m * P.G);
+      double pv[6];
+#pragma unroll
+      for (int c = 0; c < 6; ++c) pv[c] = ps[6 * nq + c];
+#pragma unroll
+      for (int i = 0; i < 6; ++i)
+#pragma unroll
+        for (int c = 0; c < 6; ++c) acc[i] += A[sym6(i, c)] * pv[c];
+    }
+    if (!act) {
+#pragma unroll
+      for (int c = 0; c < 6; ++c) pown[c] = 0.0;
+    }
+    {
+      const double pp = tile_partial(act, node_dot(pown, acc));
+      if (j == 0 && T.live) part[2 * tile] = pp;
+    }
+    __syncthreads();
+    const double pAp = pair_total_smem(part, P.ntiles, 2, red);
+    if (pAp <= 0.0) {  // solver.cpp:344-346
+      if (threadIdx.x == 0) atomicOr(a.flags + pair, kFlagCurvature);
+      stop = true;
+      break;
+    }
+    alpha = rz / pAp;
+    // k_pcg_update: x += alpha p, r -= alpha Ap, z = M r (solver.cpp:348-351)
+    if (act) {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        x[k] += alpha * pown[k];
+        r[k] -= alpha * acc[k];
+      }
+    }
+    pcg_precond(P, n, r, z);
+    {
+      const double prz = tile_partial(act, node_dot(r, z));
+      const double prr = want_rr ? tile_partial(act, node_dot(r, r)) : 0.0;
+      if (j == 0 && T.live) {
+        part[2 * tile] = prz;
+        part[2 * tile + 1] = prr;
+      }
+    }
+    __syncthreads();
+    const double rzn = pair_total_smem(part, P.ntiles, 2, red);
+    const double rr = want_rr ? pair_total_smem(part + 1, P.ntiles, 2, red) : 0.0;
+    if (threadIdx.x == 0 && P.tr) P.tr[it + 1] = sqrt(rr);
+    if (fabs(rzn) > 100.0 * rz0) {  // solver.cpp:352-355
+      if (threadIdx.x == 0) atomicOr(a.flags + pair, kFlagGrowth);
+      stop = true;
+      break;
+    }
+    beta = rzn / rz;
+    rz = rzn;
+  }
+  if (act) st6(P.x + 6 * n, x);  // the hwf_pcg seam reads x back
+  if (a.update) {  // delta += x, total = base + delta (solver.cpp:518-523), as tile_apply
+    bool bad = false;
+    if (act) {
+      const size_t o = static_cast<size_t>(pair) * 6 * P.G + 6 * n;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        bad = bad || !isfinite(x[k]);
+        if ((a.active >> (k >> 1)) & 1) a.delta[o + k] += x[k];
+        a.total[o + k] = a.base[o + k] + a.delta[o + k];
+      }
+    }
+    if (__any_sync(0xffffffffu, bad) && j == 0) atomicOr(a.flags + pair, kFlagStep);
+  }
+}
+
 }  // namespace
 
 void init_solve_attributes() {
   cudaFuncSetAttribute(k_schwarz22, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * sizeof(Swz22Smem));
+  cudaFuncSetAttribute(k_pcg_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 }
 
 void launch_schwarz(const SwzArgs& a_in, int B, cudaStream_t s) {
@@ -905,8 +1058,19 @@ dim3 pcg_grid(const PcgArgs& a, int B) {
 }
 }  // namespace
 
+#ifndef HWF_PCG_FUSED  // small levels run pcg_solve in one CTA per pair (A/B knob: 0 = per-phase kernels everywhere)
+#define HWF_PCG_FUSED 1
+#endif
+size_t pcg_fused_smem(int gw, int gh) {
+  return (static_cast<size_t>(6) * gw * gh + 2 * kFusedMaxTiles + kPcgWarps) * sizeof(double);
+}
 void launch_pcg_global(const PcgArgs& a_in, int B, cudaStream_t s) {
   const PcgArgs a = whole(a_in);
+  const int ntiles = pcg_tiles(a.gw, a.gh);
+  if (HWF_PCG_FUSED && !a.split && ntiles <= kFusedMaxTiles && pcg_fused_smem(a.gw, a.gh) <= 200 * 1024) {
+    k_pcg_fused<<<B, 32 * ntiles, pcg_fused_smem(a.gw, a.gh), s>>>(a);
+    return;
+  }
   const dim3 grid = pcg_grid(a, B);
   k_pcg_init<<<grid, kPcgThreads, 0, s>>>(a);
   for (int it = 0; it < a.iters; ++it) {
@@ -926,6 +1090,7 @@ void launch_pcg_scalars(const PcgArgs& a_in, int phase, int it, cudaStream_t s) 
   k_pcg_scalars<<<1, kPcgThreads, 0, s>>>(whole(a_in), phase, it);
 }
 int pcg_launches(int gw, int gh, int iters) {
+  if (HWF_PCG_FUSED && pcg_tiles(gw, gh) <= kFusedMaxTiles && pcg_fused_smem(gw, gh) <= 200 * 1024) return 1;
   return 1 + 2 * iters;
 }
 
