@@ -1068,7 +1068,8 @@ void launch_pcg_global(const PcgArgs& a_in, int B, cudaStream_t s) {
   const PcgArgs a = whole(a_in);
   const int ntiles = pcg_tiles(a.gw, a.gh);
   if (HWF_PCG_FUSED && !a.split && ntiles <= kFusedMaxTiles && pcg_fused_smem(a.gw, a.gh) <= 200 * 1024) {
-    k_pcg_fused<<<B, 32 * ntiles, pcg_fused_smem(a.gw, a.gh), s>>>(a);
+    // at least kPcgWarps warps: pair_total's tree reads the partial of each of the first 4 (tile-less warps add 0)
+    k_pcg_fused<<<B, 32 * std::max(ntiles, kPcgWarps), pcg_fused_smem(a.gw, a.gh), s>>>(a);
     return;
   }
   const dim3 grid = pcg_grid(a, B);
