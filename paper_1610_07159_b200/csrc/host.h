@@ -166,6 +166,7 @@ struct Energies {  // partial buffer [B][nslots][cap][5] and reduced [B][nslots]
   int nslots = 0, cap = 0;
   double* part = nullptr;
   double* red = nullptr;
+  int* count = nullptr;  // [nslots] partials a slot's level writes (<= cap; the rest stay zero), or null
   long long pair_stride() const { return static_cast<long long>(nslots) * cap * kNumEnergy; }
   double* slot(int s) const { return part + static_cast<size_t>(s) * cap * kNumEnergy; }
 };
@@ -510,6 +511,13 @@ struct Plan {
     sc.alloc(mem, B, N0, lv[0].G, true, L > 1, S.subdomain_px <= 0, pcg_tiles(lv[0].gw, lv[0].gh));
     E.nslots = std::max(nslots, 1);
     E.cap = static_cast<int>(cap);
+    {  // the reduction reads only a slot's own level's partials (coarse slots hold far fewer than cap)
+      std::vector<int> cnt(E.nslots, E.cap);
+      for (int l = 0; l < L; ++l)
+        for (int k = 0; k < 2 * gn[l]; ++k) cnt[slot_base[l] + k] = lv[l].n_pix_cta + lv[l].n_node_cta;
+      E.count = mem.alloc<int>(E.nslots);
+      CK(cudaMemcpy(E.count, cnt.data(), sizeof(int) * E.nslots, cudaMemcpyHostToDevice));
+    }
     E.part = mem.alloc<double>(static_cast<size_t>(B) * E.pair_stride());
     E.red = mem.alloc<double>(static_cast<size_t>(B) * E.nslots * kNumEnergy);
     flags = mem.alloc<int>(B);
@@ -630,7 +638,7 @@ struct Plan {
       launch_dense(lv[0].w, lv[0].h, lv[0].gw, lv[0].gh, lv[0].step, lv[0].total, B, o_s, o_m, o_d, o_disp, st);
       LC.count++;
     }
-    launch_energy_reduce(E.part, E.nslots, E.cap, B, E.red, flags, st);
+    launch_energy_reduce(E.part, E.nslots, E.cap, B, E.red, flags, st, E.count);
     LC.count++;
     CK(cudaGetLastError());
   }

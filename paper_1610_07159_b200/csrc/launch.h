@@ -164,6 +164,6 @@ void launch_propagate(int gw, int gh, int step, const double* prev_delta, const 
 void launch_dense(int w, int h, int gw, int gh, int step, const double* total, int B, double* s_out,
                   double* m_out, double* d_out, double* disp_out, cudaStream_t s);
 void launch_energy_reduce(const double* ep, int nslots, int cap, int B, double* out, int* flags,
-                          cudaStream_t s);
+                          cudaStream_t s, const int* counts = nullptr);
 
 }  // namespace hwf

@@ -671,13 +671,15 @@ __global__ void k_dense(int w, int h, int gw, int gh, int step, const double* __
 // warp per slot took 2.5 ms at 4K, where a slot holds ~160k partials.)
 constexpr int kReduceThreads = 256;
 __global__ void __launch_bounds__(kReduceThreads) k_energy_reduce(const double* __restrict__ ep, int nslots, int cap,
-                                                                  int B, double* out, int* flags) {
+                                                                  int B, double* out, int* flags,
+                                                                  const int* __restrict__ counts) {
   __shared__ double red[kReduceThreads / 32][kNumEnergy];
   const int t = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int pair = t / nslots;
   const double* p = ep + static_cast<size_t>(t) * cap * kNumEnergy;
   double s[kNumEnergy] = {0, 0, 0, 0, 0};
-  for (int i = threadIdx.x; i < cap; i += kReduceThreads)
+  const int n = counts ? counts[t % nslots] : cap;  // entries past a slot's count are the zeros of the reset
+  for (int i = threadIdx.x; i < n; i += kReduceThreads)
 #pragma unroll
     for (int k = 0; k < kNumEnergy; ++k) s[k] += p[i * kNumEnergy + k];
 #pragma unroll
@@ -807,8 +809,9 @@ void launch_dense(int w, int h, int gw, int gh, int step, const double* total, i
                   double* d_out, double* disp_out, cudaStream_t s) {
   k_dense<<<rows_grid(w, h, B), row_threads(w), 0, s>>>(w, h, gw, gh, step, total, s_out, m_out, d_out, disp_out);
 }
-void launch_energy_reduce(const double* ep, int nslots, int cap, int B, double* out, int* flags, cudaStream_t s) {
-  k_energy_reduce<<<static_cast<unsigned>(nslots * B), kReduceThreads, 0, s>>>(ep, nslots, cap, B, out, flags);
+void launch_energy_reduce(const double* ep, int nslots, int cap, int B, double* out, int* flags, cudaStream_t s,
+                          const int* counts) {
+  k_energy_reduce<<<static_cast<unsigned>(nslots * B), kReduceThreads, 0, s>>>(ep, nslots, cap, B, out, flags, counts);
 }
 
 }  // namespace hwf
