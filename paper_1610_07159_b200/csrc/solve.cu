@@ -869,6 +869,9 @@ __device__ __forceinline__ double pair_total_smem(const double* part, int n, int
   return t;
 }
 
+// SYS_SMEM (the smallest levels, whose pair's system fits): the system is staged in shared memory once and the
+// five iterations read it there.
+template <bool SYS_SMEM>
 __global__ void __launch_bounds__(32 * kFusedMaxTiles) k_pcg_fused(const PcgArgs a) {
   extern __shared__ __align__(16) double fsm[];
   const int pair = blockIdx.x, tile = threadIdx.x >> 5, j = threadIdx.x & 31;
@@ -876,16 +879,37 @@ __global__ void __launch_bounds__(32 * kFusedMaxTiles) k_pcg_fused(const PcgArgs
   double* ps = fsm;                         // p, node-major [G][6]
   double* part = fsm + 6 * P.G;             // [ntiles][2]
   double* red = part + 2 * kFusedMaxTiles;  // [kPcgWarps]
+  double* sys_s = red + kPcgWarps;          // SYS_SMEM: the pair's system, entry-major [kSysStride][G]
+  __shared__ uint64_t sys_bar;
+  if (SYS_SMEM) {  // one bulk-async (TMA) copy of the pair's contiguous 960 G bytes, completing on an mbarrier
+    if (threadIdx.x == 0) bulk::mbar_init(&sys_bar);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint32_t bytes = static_cast<uint32_t>(kSysStride * sizeof(double) * P.G);
+      bulk::mbar_expect(&sys_bar, bytes);
+      bulk::copy(sys_s, P.sys, bytes, &sys_bar);
+    }
+    bulk::mbar_wait(&sys_bar, 0);
+  }
+  const double* S = SYS_SMEM ? sys_s : P.sys;
+  auto lds = [&](const double* q) { return SYS_SMEM ? *q : __ldg(q); };
+
   const PcgTile T = pcg_tile_at(a.gw, a.gh, tile, P.ntiles);
   const bool act = j < T.width;
   const int a_ = T.a0 + min(j, max(T.width - 1, 0));
   const size_t n = static_cast<size_t>(T.b) * a.gw + a_;
   const bool want_rr = P.tr != nullptr;
+  auto precond = [&](const double (&rv)[6], double (&zv)[6]) {  // pcg_precond from S
+    double M[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) M[i] = lds(S + (kSysPre + i) * P.G + n);
+    pcg_precond_apply(M, rv, zv);
+  };
   // k_pcg_init
   double r[6], z[6], x[6] = {0, 0, 0, 0, 0, 0};
 #pragma unroll
-  for (int k = 0; k < 6; ++k) r[k] = act ? __ldg(P.sys + (kSysRhs + k) * P.G + n) : 0.0;
-  pcg_precond(P, n, r, z);  // (the preconditioner is re-read per update: L2 hits, fewer live registers)
+  for (int k = 0; k < 6; ++k) r[k] = act ? lds(S + (kSysRhs + k) * P.G + n) : 0.0;
+  precond(r, z);  // (the preconditioner is re-read per update: fewer live registers)
   for (int i = threadIdx.x; i < 6 * static_cast<int>(P.G); i += blockDim.x) ps[i] = 0.0;  // p_prev = 0
   {
     const double prz = tile_partial(act, node_dot(r, z)), prr = tile_partial(act, node_dot(r, r));
@@ -925,10 +949,10 @@ __global__ void __launch_bounds__(32 * kFusedMaxTiles) k_pcg_fused(const PcgArgs
       const int qa = a_ + dx, qb = T.b + dy;
       if (!(act && qa >= 0 && qa < a.gw && qb >= 0 && qb < a.gh)) continue;
       const size_t nq = static_cast<size_t>(qb) * a.gw + qa;
-      const double* blk = P.sys + static_cast<size_t>(s9 >= 4 ? s9 - 4 : 4 - s9) * 21 * P.G + (s9 >= 4 ? n : nq);
+      const double* blk = S + static_cast<size_t>(s9 >= 4 ? s9 - 4 : 4 - s9) * 21 * P.G + (s9 >= 4 ? n : nq);
       double A[21];
 #pragma unroll
-      for (int m = 0; m < 21; ++m) A[m] = __ldg(blk + m * P.G);
+      for (int m = 0; m < 21; ++m) A[m] = lds(blk + m * P.G);
       double pv[6];
 #pragma unroll
       for (int c = 0; c < 6; ++c) pv[c] = ps[6 * nq + c];
@@ -961,7 +985,7 @@ __global__ void __launch_bounds__(32 * kFusedMaxTiles) k_pcg_fused(const PcgArgs
         r[k] -= alpha * acc[k];
       }
     }
-    pcg_precond(P, n, r, z);
+    precond(r, z);
     {
       const double prz = tile_partial(act, node_dot(r, z));
       const double prr = want_rr ? tile_partial(act, node_dot(r, r)) : 0.0;
@@ -1002,7 +1026,8 @@ __global__ void __launch_bounds__(32 * kFusedMaxTiles) k_pcg_fused(const PcgArgs
 
 void init_solve_attributes() {
   cudaFuncSetAttribute(k_schwarz22, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * sizeof(Swz22Smem));
-  cudaFuncSetAttribute(k_pcg_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_pcg_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_pcg_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 }
 
 void launch_schwarz(const SwzArgs& a_in, int B, cudaStream_t s) {
@@ -1061,15 +1086,22 @@ dim3 pcg_grid(const PcgArgs& a, int B) {
 #ifndef HWF_PCG_FUSED  // small levels run pcg_solve in one CTA per pair (A/B knob: 0 = per-phase kernels everywhere)
 #define HWF_PCG_FUSED 1
 #endif
-size_t pcg_fused_smem(int gw, int gh) {
-  return (static_cast<size_t>(6) * gw * gh + 2 * kFusedMaxTiles + kPcgWarps) * sizeof(double);
+#ifndef HWF_PCG_SYS_SMEM  // ... with the pair's system staged in shared memory when it fits (A/B knob)
+#define HWF_PCG_SYS_SMEM 1
+#endif
+size_t pcg_fused_smem(int gw, int gh, bool sys_smem = false) {
+  return (static_cast<size_t>(6 + (sys_smem ? kSysStride : 0)) * gw * gh + 2 * kFusedMaxTiles + kPcgWarps) *
+         sizeof(double);
 }
 void launch_pcg_global(const PcgArgs& a_in, int B, cudaStream_t s) {
   const PcgArgs a = whole(a_in);
   const int ntiles = pcg_tiles(a.gw, a.gh);
   if (HWF_PCG_FUSED && !a.split && ntiles <= kFusedMaxTiles && pcg_fused_smem(a.gw, a.gh) <= 200 * 1024) {
     // at least kPcgWarps warps: pair_total's tree reads the partial of each of the first 4 (tile-less warps add 0)
-    k_pcg_fused<<<B, 32 * std::max(ntiles, kPcgWarps), pcg_fused_smem(a.gw, a.gh), s>>>(a);
+    if (HWF_PCG_SYS_SMEM && pcg_fused_smem(a.gw, a.gh, true) <= 200 * 1024)
+      k_pcg_fused<true><<<B, 32 * std::max(ntiles, kPcgWarps), pcg_fused_smem(a.gw, a.gh, true), s>>>(a);
+    else
+      k_pcg_fused<false><<<B, 32 * std::max(ntiles, kPcgWarps), pcg_fused_smem(a.gw, a.gh), s>>>(a);
     return;
   }
   const dim3 grid = pcg_grid(a, B);
