@@ -7,7 +7,9 @@ solve. The oracle poisons every published row a rank should not know, so a missi
 exchange fails.
 -m gpu: the device split (csrc/split.cu) with in-process ranks sharing one context, against
 the unsplit device solve. The ranks are stepped by the host, and no kernel waits on
-another rank. Also the NCCL path with world_size 1.
+another rank. Also the NCCL path with world_size 1. The unsplit solve runs the small levels'
+PCG in one CTA per pair (k_pcg_fused) while the split runs the per-phase kernels, so the
+bitwise comparisons also pin the fused kernel to the per-phase arithmetic.
 """
 from __future__ import annotations
 
