@@ -501,6 +501,15 @@ def run_ours(args, ws, rank, local):
             "ms_per_gn_iter": ms_per_step / gn_total / B,  # whole step per pair per GN iteration (amortised)
             "gn_iter_by_level": gn_iter,  # measured: one GN iteration (linearise + solve) of the B-pair batch
             "hbm_gbs": achieved,  # dominant kernel, algorithmic bytes / CUDA-event time
+            # the whole pipeline against SURVEY.md §8(d)'s streaming model of cfg2 (~271 MB and ~3.45 GFLOP per pair):
+            # the HBM-bound and FP64-bound pair rates, and this run's fraction of each
+            "pipeline_model": {"bytes_per_pair": 271e6, "flop_per_pair": 3.45e9,
+                               "hbm_pairs_per_s": pk["hbm_gbs"] * 1e9 / 271e6,
+                               "hbm_frac": value * 271e6 / (pk["hbm_gbs"] * 1e9) / ws if pk["hbm_gbs"] else None,
+                               "fp64_pairs_per_s": (fp64["peak"] * 1e12 / 3.45e9) if fp64 else None,
+                               "fp64_frac": (value / ws * 3.45e9 / (fp64["peak"] * 1e12)) if fp64 else None,
+                               "src": "SURVEY.md §8(d) streaming model; peaks: MEASURED_PEAKS.json hbm_gbs, "
+                                      "profiles/fp64_peak.json"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"] if pk["hbm_gbs"] else None, "traffic": traffic,
                          "kernel": "k_pixel<LIN,U8> (fused data term + cell reduction), finest level, u8 frames sampled directly",
