@@ -474,3 +474,42 @@ def test_jacobian_finite_differences(device, oracle):
     for s in (device, oracle):
         errs = _fd_jacobian_check(s, lv, EnergyParams.preset("facial"), picks)
         assert np.median(errs) < 1e-5 and (errs < 1e-3).mean() >= 0.9, errs
+
+
+@pytest.mark.parametrize("gw,gh", [(3, 2), (32, 16), (33, 17)])  # fused (<= 16 tiles, system in smem), fused, per-phase
+def test_pcg_device_edge_cases_match_oracle(device, oracle, gw, gh):
+    """hwf_pcg on both device paths (k_pcg_fused for <= 16 tiles per pair, the per-phase kernels above): SPEC.md:330-331
+    identity / diagonal systems solve in one iteration, a zero rhs returns x = 0 with a zero trace (solver.cpp:334-338),
+    a random SPD system matches the oracle with its trace, and an indefinite one raises SolverDivergence as the
+    oracle does (pAp <= 0, solver.cpp:344-346)."""
+    G = gw * gh
+    rng = np.random.default_rng(gw * 100 + gh)
+    b = rng.normal(size=6 * G)
+    blocks = np.zeros((G, 9, 6, 6))
+    blocks[:, 4] = np.eye(6)
+    np.testing.assert_allclose(device.pcg_solve(gw, gh, blocks, b, 1), b, rtol=1e-14)
+    blocks[:, 4] = np.diag(np.arange(1.0, 7.0))
+    np.testing.assert_allclose(device.pcg_solve(gw, gh, blocks, b, 1), b / np.tile(np.arange(1.0, 7.0), G), rtol=1e-13)
+    x, tr = device.pcg_solve(gw, gh, blocks, np.zeros(6 * G), 4, trace=True)
+    assert not x.any() and not np.asarray(tr).any()
+    # SPD: diagonally dominant, with symmetric coupling blocks (every block of this system is a sum of a a' J J^T, and
+    # the device keeps 21 packed entries per block), mirrored as NormalSystem stores them
+    spd = np.zeros((G, 9, 6, 6))
+    for n in range(G):
+        a, bb = n % gw, n // gw
+        spd[n, 4] = np.eye(6) * 40.0 + 0.5 * (lambda m: m + m.T)(rng.normal(size=(6, 6)))
+        for s9 in (5, 6, 7, 8):  # forward slots; the backward ones mirror them
+            dx, dy = s9 % 3 - 1, s9 // 3 - 1
+            if 0 <= a + dx < gw and bb + dy < gh:
+                m = (lambda r: 0.5 * (r + r.T))(rng.normal(size=(6, 6)))
+                spd[n, s9] = m
+                spd[n + dy * gw + dx, 8 - s9] = m.T
+    xd, td = device.pcg_solve(gw, gh, spd, b, 6, trace=True)
+    xo, to = oracle.pcg_solve(gw, gh, spd, b, 6, trace=True)
+    np.testing.assert_allclose(xd, xo, rtol=1e-10, atol=1e-12 * np.abs(xo).max())
+    np.testing.assert_allclose(td, to, rtol=1e-10)
+    bad = spd.copy()
+    bad[:, 4] = -np.eye(6) * 40.0  # negative definite diagonal: the first p.Ap is negative
+    for solver in (oracle, device):
+        with pytest.raises(SolverDivergence):
+            solver.pcg_solve(gw, gh, bad, b, 6)
