@@ -170,6 +170,33 @@ def test_illumination_matches_oracle(device, oracle):
     np.testing.assert_allclose(ha, hb, rtol=0, atol=1e-12)
 
 
+@pytest.mark.parametrize("w,h,step", [(97, 61, 8), (23, 17, 4), (330, 20, 8), (161, 9, 2)])
+def test_illumination_ragged_widths(device, oracle, w, h, step):
+    """The windowed blur (160-wide row segments, 8-row column windows) on widths and heights that are not multiples
+    of either, including rows shorter than the 10 px radius."""
+    lv = _random_level(w + h, w, h, step)
+    vis = oracle.compute_occlusion_maps(w, h, step, lv.total)
+    ha = device.compute_illumination_maps(lv.images, step, lv.total, vis)
+    hb = oracle.compute_illumination_maps(lv.images, step, lv.total, vis)
+    np.testing.assert_allclose(ha, hb, rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("wc,hc,wf,hf,step", [(40, 30, 80, 60, 8), (21, 11, 41, 21, 4), (3, 2, 5, 3, 2),
+                                             (160, 120, 320, 240, 8), (1, 7, 2, 13, 1)])
+def test_mask_prolongation_bit_exact(device, oracle, wc, hc, wf, hf, step):
+    """Masks alone (the pipeline's k_prolong_vis: 4 pixels per thread, the quarter-weight vote as bitwise ops), on
+    fine widths that are not multiples of 4 and single-column coarse levels."""
+    rng = np.random.default_rng(wc * 7 + hf)
+    gwc, ghc = grid_dims(wc, hc, step)
+    tc = rng.normal(0, 2, (gwc * ghc, 6))
+    vc = rng.integers(0, 16, (hc, wc)).astype(np.uint8)
+    a = device.prolongate(wc, hc, wf, hf, step, tc, vc, None)
+    b = oracle.prolongate(wc, hc, wf, hf, step, tc, vc, None)
+    for x, y in zip(a, b):
+        if x is not None or y is not None:
+            assert np.array_equal(x, y)
+
+
 def test_prolongation_bit_exact(device, oracle):
     rng = np.random.default_rng(2)
     for (wc, hc, wf, hf, step) in ((40, 30, 80, 60, 8), (21, 11, 41, 21, 4), (160, 120, 320, 240, 8)):
